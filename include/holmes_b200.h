@@ -1,0 +1,127 @@
+/* holmes_b200.h — C ABI of the B200 ensemble-serving hot path.
+ *
+ * The reference (zooserve, pure Python) has no FFI: its plug points are Python
+ * callables.  Each entry point below replaces one of them; the Python mirror in
+ * paper_2008_04063_b200/ binds them with ctypes (INTEGRATION.md shows the
+ * binding a zooserve maintainer would add).
+ *
+ *   hb_create / hb_add_member / hb_set_selector
+ *       replace the zoo + selector bookkeeping of `_WindowScorer.__init__`
+ *       (pkg/src/zooserve/runtime.py:121-129) and `_check_modalities`
+ *       (runtime.py:139-147): members are real 1-D ResNets (arch.py), the
+ *       selector is the ensemble bitmask (zoo.py:80-136).
+ *   hb_ingest
+ *       replaces `Aggregator.add` (runtime.py:98-115) for a whole tick of all
+ *       (patient, lead) streams at once: samples go into device ring buffers.
+ *   hb_tick
+ *       replaces `_WindowScorer.draw` (runtime.py:131-136) + `service_time`
+ *       (latency.py:145-151): window gather/z-norm, every selected member's
+ *       forward, and the ensemble aggregate, for all patients, per tick.
+ *   hb_sweep_auc
+ *       replaces `exhaustive_search`'s batched accuracy pass
+ *       `roc_auc_many(labels, scores @ bits.T / pop)` (composer.py:614-619,
+ *       metrics.py:30-76) with exact midrank AUCs.
+ *
+ * Conventions: every call returns an hb_status; 0 = ok.  Non-zero codes map
+ * onto the reference's exception classes (errors.py): HB_E_INVALID ->
+ * ValueError, HB_E_CONFIG -> ConfigurationError, HB_E_EMPTY ->
+ * EmptyEnsembleError, HB_E_METRIC -> UndefinedMetricError.  The caller owns
+ * host buffers; the context owns device memory.  All work is stream-ordered;
+ * `stream` is a cudaStream_t passed as void* (NULL = the context's own
+ * stream).  A context is not thread-safe (the Python side holds a lock, as
+ * the reference's wall-clock mode does around the scorer, runtime.py:367-368).
+ * There is no CPU fallback: without a CUDA device every call fails.
+ */
+#ifndef HOLMES_B200_H
+#define HOLMES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HB_OK = 0,
+  HB_E_INVALID = 1, /* ValueError */
+  HB_E_CONFIG = 2,  /* ConfigurationError */
+  HB_E_EMPTY = 3,   /* EmptyEnsembleError */
+  HB_E_CUDA = 4,    /* device failure (DeviceError) */
+  HB_E_STATE = 5,   /* call order violated */
+  HB_E_METRIC = 6   /* UndefinedMetricError */
+} hb_status;
+
+typedef struct hb_ctx hb_ctx;
+
+typedef struct {
+  int max_patients; /* P: streams are [P][n_leads] */
+  int n_leads;      /* ECG leads per patient (3) */
+  int fs;           /* sampling rate, Hz (250) */
+  int window_len;   /* samples per window (fs * window_s = 7500) */
+  int hop;          /* samples appended per tick (250 = 1 s tick; == window_len: tumbling) */
+  int ring_len;     /* ring buffer length per stream (>= window_len; 0 = auto) */
+  int keep_windows; /* 1 = retain each tick's raw windows for hb_last_windows (diagnostics) */
+} hb_config;
+
+int hb_version(void);
+/* Last error message of ctx, or of the calling thread's last failed hb_create when ctx is NULL. */
+const char* hb_last_error(const hb_ctx* ctx);
+
+int hb_create(int device, const hb_config* cfg, hb_ctx** out);
+int hb_destroy(hb_ctx* ctx);
+
+/* Register zoo member `idx` (zoo order) reading lead `lead` (0-based) with the
+ * architecture of ModelProfile(width, depth).  `params` is the flat fp32 blob of
+ * arch.flatten_params: per conv layer W[cout][cin][16] then bias[cout] (BN
+ * folded), in execution order, then fc_w[c_last], fc_b[1].  Weights are
+ * converted to fp16 tensor-core operands on the device. */
+int hb_add_member(hb_ctx* ctx, int idx, int lead, int width, int depth, const float* params, size_t n_floats);
+
+/* Ensemble selector: bits[n], bit k <-> member idx k.  Members must be registered. */
+int hb_set_selector(hb_ctx* ctx, const uint8_t* bits, int n);
+/* Number of members the current selector runs (M) and their idx order. */
+int hb_selected(const hb_ctx* ctx, int* idx_out, int cap);
+
+/* Append n_per_stream samples [P][n_leads][n_per_stream] (host, fp32) without scoring. */
+int hb_ingest(hb_ctx* ctx, const float* samples, int n_per_stream, void* stream);
+
+/* One serving tick: append `hop` new samples per stream from host `samples`
+ * ([P][n_leads][hop] fp32; NULL = already staged with hb_stage_device), score
+ * the latest window of every patient with every selected member, aggregate.
+ * Outputs (host, may be NULL): member_logits[P][M] (selected order),
+ * ens_prob[P] = mean of member sigmoids, ens_mean_logit[P] = mean member logit.
+ * With host outputs the call synchronises `stream` before returning. */
+int hb_tick(hb_ctx* ctx, const float* samples, float* member_logits, float* ens_prob, float* ens_mean_logit,
+            void* stream);
+
+/* Device-resident variants (benchmarks, zero-copy callers): copy a device
+ * buffer [P][n_leads][hop] into the staging area; outputs stay on device. */
+int hb_stage_device(hb_ctx* ctx, const float* dev_samples, void* stream);
+int hb_tick_device(hb_ctx* ctx, void* stream);
+int hb_device_outputs(const hb_ctx* ctx, float** member_logits, float** ens_prob, float** ens_mean_logit);
+
+/* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
+ * (mean, std) [P][n_leads][2] of the most recent tick. */
+int hb_last_windows(hb_ctx* ctx, float* raw, float* stats, void* stream);
+/* Algorithmic work of one tick: conv FLOPs and activation bytes (all selected members). */
+int hb_tick_work(const hb_ctx* ctx, double* flops, double* bytes);
+
+/* Profiler sweep: exact ROC-AUC (Mann-Whitney U from midranks, ties half
+ * credit) of the ensemble mean scores[:, sel].mean(1) for every selector.
+ * scores [N][n] fp64 row-major, labels[N] in {0,1}, selectors[S] bitmasks
+ * (bit k <-> column k, n <= 32).  Host buffers in and out. */
+int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
+                 int S, double* auc_out);
+
+/* Kernel-level entry points used by the parity tests (device pointers). */
+int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
+                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, const float* fc_w_host,
+                 float* head_out, void* stream);
+int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,561 @@
+// C-ABI layer (include/holmes_b200.h): the serving context, member registry,
+// per-tick CUDA graph (ingest/window -> members' stem + tcgen05 convs ->
+// aggregate -> cursor advance), and kernel-level test entry points.
+#include "../../include/holmes_b200.h"
+#include "hb_kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+using namespace hb;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct LayerSpec {
+  int cin, cout, stride, lin, lout, pad, res_mode, res_c, head;
+};
+
+// Same table as paper_2008_04063_b200/arch.py:member_layers (stem first).
+std::vector<LayerSpec> member_layers(int width, int depth, int window) {
+  std::vector<LayerSpec> v;
+  auto same = [](int lin, int s, int* lout, int* pad) {
+    *lout = (lin + s - 1) / s;
+    const int tot = (*lout - 1) * s + kTaps - lin;
+    *pad = tot > 0 ? tot / 2 : 0;
+  };
+  int lo, pd;
+  same(window, 1, &lo, &pd);
+  v.push_back({1, width, 1, window, lo, pd, 0, 0, 0});
+  int len = window;
+  for (int i = 0; i < depth; ++i) {
+    const int s = (i % 2 == 1) ? 2 : 1;
+    const int cin = (i == 0) ? width : width * (1 << ((i - 1) / 4));
+    const int cout = (i % 4 == 0 && i > 0) ? 2 * cin : cin;
+    int l1, p1, l2, p2;
+    same(len, s, &l1, &p1);
+    same(l1, 1, &l2, &p2);
+    v.push_back({cin, cout, s, len, l1, p1, 0, 0, 0});
+    v.push_back({cout, cout, 1, l1, l2, p2, s == 2 ? 2 : 1, cin, i == depth - 1 ? 1 : 0});
+    len = l2;
+  }
+  return v;
+}
+
+struct Member {
+  int idx = -1, lead = 0, width = 0, depth = 0;
+  std::vector<LayerSpec> layers;
+  float* stem_w = nullptr;  // [w][16]
+  float* stem_b = nullptr;
+  std::vector<uint8_t*> wpack;  // per conv layer (layers[1..])
+  std::vector<float*> bias;
+  float* fc_w = nullptr;
+  float fc_b = 0.f;
+  float* head_partial = nullptr;  // [P][mt]
+  int head_mt = 0;
+  double flops = 0, bytes = 0;
+};
+
+}  // namespace
+
+struct hb_ctx {
+  int device = 0, P = 0, leads = 0, fs = 0, W = 0, hop = 0, R = 0, keep = 0, num_sms = 148;
+  cudaStream_t own = nullptr;
+  float* ring = nullptr;
+  float* staged = nullptr;   // [P][leads][hop]
+  float* prefill = nullptr;  // [P][leads][R]
+  long long* wpos = nullptr;
+  __half* xn = nullptr;      // [leads][P][W]
+  float* raw = nullptr;      // [P][leads][W] (keep_windows)
+  float* stats = nullptr;    // [P][leads][2]
+  std::map<int, Member> members;
+  std::vector<int> selected;
+  // per-selection resources
+  __half* act[3] = {nullptr, nullptr, nullptr};
+  size_t act_bytes = 0;
+  HeadMember* d_heads = nullptr;
+  float* member_logits = nullptr;
+  float* ens_prob = nullptr;
+  float* ens_logit = nullptr;
+  std::vector<ConvPlan> plans;
+  cudaGraphExec_t graph = nullptr;
+  bool dirty = true;
+  std::string err;
+};
+
+namespace {
+
+int fail(hb_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg; else g_create_err = msg;
+  return code;
+}
+
+#define CK(c, expr)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail(c, HB_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+cudaStream_t pick(hb_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->own; }
+
+void free_selection(hb_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
+  for (auto& a : c->act) {
+    if (a) cudaFree(a);
+    a = nullptr;
+  }
+  c->act_bytes = 0;
+  if (c->d_heads) cudaFree(c->d_heads);
+  if (c->member_logits) cudaFree(c->member_logits);
+  if (c->ens_prob) cudaFree(c->ens_prob);
+  if (c->ens_logit) cudaFree(c->ens_logit);
+  c->d_heads = nullptr;
+  c->member_logits = c->ens_prob = c->ens_logit = nullptr;
+  c->plans.clear();
+}
+
+void free_member(Member& m) {
+  cudaFree(m.stem_w);
+  cudaFree(m.stem_b);
+  for (auto p : m.wpack) cudaFree(p);
+  for (auto p : m.bias) cudaFree(p);
+  cudaFree(m.fc_w);
+  cudaFree(m.head_partial);
+}
+
+// Enqueue the whole tick (after staging) on stream st.
+int enqueue_tick(hb_ctx* c, cudaStream_t st) {
+  CK(c, launch_ingest_window(c->staged, c->ring, c->wpos, c->P, c->leads, c->hop, c->R, c->W, c->xn,
+                             c->keep ? c->raw : nullptr, c->stats, st));
+  size_t pi = 0;
+  for (int idx : c->selected) {
+    Member& m = c->members[idx];
+    const LayerSpec& s0 = m.layers[0];
+    CK(c, launch_stem(c->xn + static_cast<size_t>(m.lead) * c->P * c->W, c->W, c->P, c->W,
+                      round_up(s0.lout, 8), s0.cout, s0.pad, m.stem_w, m.stem_b, c->act[0], st));
+    for (size_t li = 1; li < m.layers.size(); ++li) CK(c, launch_conv(c->plans[pi++], st));
+  }
+  CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
+                         c->ens_logit, st));
+  CK(c, launch_advance(c->wpos, c->hop, st));
+  return HB_OK;
+}
+
+int build_selection(hb_ctx* c) {
+  if (!c->dirty) return HB_OK;
+  free_selection(c);
+  if (c->selected.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
+  // activation buffers sized for the largest layer output of any selected member
+  size_t need = 0;
+  for (int idx : c->selected)
+    for (auto& L : c->members[idx].layers)
+      need = std::max(need, static_cast<size_t>(c->P) * L.cout * round_up(L.lout, 8) * sizeof(__half));
+  for (auto& a : c->act) {
+    CK(c, cudaMalloc(&a, need));
+    CK(c, cudaMemset(a, 0, need));
+  }
+  c->act_bytes = need;
+  const int M = static_cast<int>(c->selected.size());
+  CK(c, cudaMalloc(&c->member_logits, sizeof(float) * c->P * M));
+  CK(c, cudaMalloc(&c->ens_prob, sizeof(float) * c->P));
+  CK(c, cudaMalloc(&c->ens_logit, sizeof(float) * c->P));
+  std::vector<HeadMember> heads;
+  for (int idx : c->selected) {
+    Member& m = c->members[idx];
+    int cur = 0;
+    for (size_t li = 1; li < m.layers.size(); ++li) {
+      const LayerSpec& L = m.layers[li];
+      const bool conv1 = (li % 2 == 1);
+      int src = cur, dst;
+      const __half* res = nullptr;
+      int res_lp = 0;
+      if (conv1) {
+        dst = (cur + 1) % 3;
+      } else {
+        src = (cur + 1) % 3;
+        dst = (cur + 2) % 3;
+        res = c->act[cur];
+        res_lp = round_up(m.layers[li - 1].lin, 8);
+      }
+      ConvPlan plan;
+      const char* e = plan_conv(&plan, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, c->act[src],
+                                round_up(L.lin, 8), L.head ? nullptr : c->act[dst], m.wpack[li - 1], m.bias[li - 1],
+                                res, conv1 ? 0 : L.res_mode, L.res_c, res_lp, L.head ? m.fc_w : nullptr,
+                                L.head ? m.head_partial : nullptr, c->num_sms);
+      if (e) return fail(c, HB_E_INVALID, e);
+      c->plans.push_back(plan);
+      if (!conv1) cur = dst;
+    }
+    heads.push_back({m.head_partial, m.head_mt, 1.f / static_cast<float>(m.layers.back().lout), m.fc_b});
+  }
+  CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
+  CK(c, cudaMemcpy(c->d_heads, heads.data(), sizeof(HeadMember) * heads.size(), cudaMemcpyHostToDevice));
+  // capture the tick into a graph
+  cudaStream_t cap;
+  CK(c, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue_tick(c, cap);
+  cudaError_t ec = cudaStreamEndCapture(cap, &g);
+  if (rc != HB_OK) {
+    cudaStreamDestroy(cap);
+    return rc;
+  }
+  CK(c, ec);
+  CK(c, cudaGraphInstantiate(&c->graph, g, 0));
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cap);
+  c->dirty = false;
+  return HB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hb_version(void) { return 1; }
+
+const char* hb_last_error(const hb_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
+  if (!cfg || !out) return fail(nullptr, HB_E_INVALID, "null argument");
+  if (cfg->max_patients < 1) return fail(nullptr, HB_E_CONFIG, "patients must be >= 1");
+  if (cfg->n_leads < 1) return fail(nullptr, HB_E_CONFIG, "n_leads must be >= 1");
+  if (cfg->window_len < kTaps) return fail(nullptr, HB_E_CONFIG, "window_len too short");
+  if (cfg->hop < 1 || cfg->hop > cfg->window_len) return fail(nullptr, HB_E_CONFIG, "hop must be in [1, window_len]");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, HB_E_CUDA, "no CUDA device (there is no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(nullptr, HB_E_INVALID, "device ordinal out of range");
+  if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, HB_E_CUDA, "cudaSetDevice failed");
+  if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
+  hb_ctx* c = new hb_ctx();
+  c->device = device;
+  c->P = cfg->max_patients;
+  c->leads = cfg->n_leads;
+  c->fs = cfg->fs;
+  c->W = cfg->window_len;
+  c->hop = cfg->hop;
+  c->R = cfg->ring_len > 0 ? cfg->ring_len : round_up(cfg->window_len + cfg->hop, 256);
+  c->keep = cfg->keep_windows;
+  if (c->R < c->W) {
+    delete c;
+    return fail(nullptr, HB_E_CONFIG, "ring_len must be >= window_len");
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t S = static_cast<size_t>(c->P) * c->leads;
+  bool ok = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMalloc(&c->ring, S * c->R * sizeof(float)) == cudaSuccess &&
+            cudaMemset(c->ring, 0, S * c->R * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->staged, S * c->hop * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->prefill, S * c->R * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->wpos, sizeof(long long)) == cudaSuccess &&
+            cudaMemset(c->wpos, 0, sizeof(long long)) == cudaSuccess &&
+            cudaMalloc(&c->xn, S * c->W * sizeof(__half)) == cudaSuccess &&
+            cudaMalloc(&c->stats, S * 2 * sizeof(float)) == cudaSuccess;
+  if (ok && c->keep) ok = cudaMalloc(&c->raw, S * c->W * sizeof(float)) == cudaSuccess;
+  if (!ok) {
+    hb_destroy(c);
+    return fail(nullptr, HB_E_CUDA, "device allocation failed");
+  }
+  *out = c;
+  return HB_OK;
+}
+
+int hb_destroy(hb_ctx* c) {
+  if (!c) return HB_OK;
+  cudaSetDevice(c->device);
+  if (c->own) cudaStreamSynchronize(c->own);
+  free_selection(c);
+  for (auto& kv : c->members) free_member(kv.second);
+  cudaFree(c->ring);
+  cudaFree(c->staged);
+  cudaFree(c->prefill);
+  cudaFree(c->wpos);
+  cudaFree(c->xn);
+  cudaFree(c->raw);
+  cudaFree(c->stats);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return HB_OK;
+}
+
+int hb_add_member(hb_ctx* c, int idx, int lead, int width, int depth, const float* params, size_t n_floats) {
+  if (!c || !params) return fail(c, HB_E_INVALID, "null argument");
+  if (idx < 0) return fail(c, HB_E_INVALID, "member idx must be >= 0");
+  if (lead < 0 || lead >= c->leads)
+    return fail(c, HB_E_CONFIG, "rates: no stream configured for lead " + std::to_string(lead));
+  if (width < 8 || width % 8 || width > 128 || depth < 1) return fail(c, HB_E_INVALID, "unsupported width/depth");
+  cudaSetDevice(c->device);
+  Member m;
+  m.idx = idx;
+  m.lead = lead;
+  m.width = width;
+  m.depth = depth;
+  m.layers = member_layers(width, depth, c->W);
+  size_t need = 0;
+  for (auto& L : m.layers) need += static_cast<size_t>(L.cout) * L.cin * kTaps + L.cout;
+  const int c_last = m.layers.back().cout;
+  need += c_last + 1;
+  if (n_floats != need)
+    return fail(c, HB_E_INVALID, "params blob has " + std::to_string(n_floats) + " floats, expected " +
+                                     std::to_string(need));
+  const float* p = params;
+  const LayerSpec& s0 = m.layers[0];
+  CK(c, cudaMalloc(&m.stem_w, sizeof(float) * s0.cout * kTaps));
+  CK(c, cudaMemcpy(m.stem_w, p, sizeof(float) * s0.cout * kTaps, cudaMemcpyHostToDevice));
+  p += s0.cout * kTaps;
+  CK(c, cudaMalloc(&m.stem_b, sizeof(float) * s0.cout));
+  CK(c, cudaMemcpy(m.stem_b, p, sizeof(float) * s0.cout, cudaMemcpyHostToDevice));
+  p += s0.cout;
+  for (size_t li = 1; li < m.layers.size(); ++li) {
+    const LayerSpec& L = m.layers[li];
+    const size_t wb = wpack_bytes(L.cin, L.cout);
+    std::vector<uint16_t> img(wb / 2);
+    pack_weights(p, L.cin, L.cout, L.stride, img.data());
+    uint8_t* dw;
+    CK(c, cudaMalloc(&dw, wb));
+    CK(c, cudaMemcpy(dw, img.data(), wb, cudaMemcpyHostToDevice));
+    m.wpack.push_back(dw);
+    p += static_cast<size_t>(L.cout) * L.cin * kTaps;
+    const int bn = conv_bn(L.cout);
+    const int nbias = ((round_up(L.cout, 16) + bn - 1) / bn) * bn;
+    std::vector<float> bias(nbias, 0.f);
+    std::copy(p, p + L.cout, bias.begin());
+    float* db;
+    CK(c, cudaMalloc(&db, sizeof(float) * nbias));
+    CK(c, cudaMemcpy(db, bias.data(), sizeof(float) * nbias, cudaMemcpyHostToDevice));
+    m.bias.push_back(db);
+    p += L.cout;
+  }
+  CK(c, cudaMalloc(&m.fc_w, sizeof(float) * c_last));
+  CK(c, cudaMemcpy(m.fc_w, p, sizeof(float) * c_last, cudaMemcpyHostToDevice));
+  p += c_last;
+  m.fc_b = *p;
+  m.head_mt = (m.layers.back().lout + kBM - 1) / kBM;
+  CK(c, cudaMalloc(&m.head_partial, sizeof(float) * c->P * m.head_mt));
+  for (auto& L : m.layers) {
+    m.flops += 2.0 * L.cin * L.cout * kTaps * L.lout;
+    m.bytes += 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout));
+  }
+  auto it = c->members.find(idx);
+  if (it != c->members.end()) free_member(it->second);
+  c->members[idx] = m;
+  c->dirty = true;
+  return HB_OK;
+}
+
+int hb_set_selector(hb_ctx* c, const uint8_t* bits, int n) {
+  if (!c || !bits) return fail(c, HB_E_INVALID, "null argument");
+  std::vector<int> sel;
+  for (int k = 0; k < n; ++k) {
+    if (bits[k] > 1) return fail(c, HB_E_INVALID, "selector bits must be 0 or 1");
+    if (bits[k]) {
+      if (!c->members.count(k)) return fail(c, HB_E_STATE, "selected member " + std::to_string(k) + " not registered");
+      sel.push_back(k);
+    }
+  }
+  if (sel.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
+  if (static_cast<int>(sel.size()) > kMaxMembers) return fail(c, HB_E_INVALID, "too many selected members");
+  if (sel != c->selected) {
+    c->selected = sel;
+    c->dirty = true;
+  }
+  return HB_OK;
+}
+
+int hb_selected(const hb_ctx* c, int* idx_out, int cap) {
+  if (!c) return -1;
+  const int M = static_cast<int>(c->selected.size());
+  for (int i = 0; i < M && i < cap && idx_out; ++i) idx_out[i] = c->selected[i];
+  return M;
+}
+
+int hb_ingest(hb_ctx* c, const float* samples, int n, void* stream) {
+  if (!c || (!samples && n > 0)) return fail(c, HB_E_INVALID, "null argument");
+  if (n < 0) return fail(c, HB_E_INVALID, "n_per_stream must be >= 0");
+  cudaSetDevice(c->device);
+  cudaStream_t st = pick(c, stream);
+  const size_t S = static_cast<size_t>(c->P) * c->leads;
+  for (int done = 0; done < n;) {
+    const int chunk = std::min(n - done, c->R);
+    // gather columns [done, done+chunk) of every stream into the contiguous prefill buffer
+    CK(c, cudaMemcpy2DAsync(c->prefill, sizeof(float) * chunk, samples + done, sizeof(float) * n,
+                            sizeof(float) * chunk, S, cudaMemcpyHostToDevice, st));
+    CK(c, launch_ingest_window(c->prefill, c->ring, c->wpos, c->P, c->leads, chunk, c->R, c->W, nullptr, nullptr,
+                               nullptr, st));
+    CK(c, launch_advance(c->wpos, chunk, st));
+    done += chunk;
+  }
+  CK(c, cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+int hb_stage_device(hb_ctx* c, const float* dev, void* stream) {
+  if (!c || !dev) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  CK(c, cudaMemcpyAsync(c->staged, dev, sizeof(float) * c->P * c->leads * c->hop, cudaMemcpyDeviceToDevice,
+                        pick(c, stream)));
+  return HB_OK;
+}
+
+int hb_tick_device(hb_ctx* c, void* stream) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  const int rc = build_selection(c);
+  if (rc) return rc;
+  CK(c, cudaGraphLaunch(c->graph, pick(c, stream)));
+  return HB_OK;
+}
+
+int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_prob, float* ens_mean_logit,
+            void* stream) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  cudaStream_t st = pick(c, stream);
+  const int rc = build_selection(c);
+  if (rc) return rc;
+  if (samples)
+    CK(c, cudaMemcpyAsync(c->staged, samples, sizeof(float) * c->P * c->leads * c->hop, cudaMemcpyHostToDevice, st));
+  CK(c, cudaGraphLaunch(c->graph, st));
+  const size_t M = c->selected.size();
+  bool any = false;
+  if (member_logits) {
+    CK(c, cudaMemcpyAsync(member_logits, c->member_logits, sizeof(float) * c->P * M, cudaMemcpyDeviceToHost, st));
+    any = true;
+  }
+  if (ens_prob) {
+    CK(c, cudaMemcpyAsync(ens_prob, c->ens_prob, sizeof(float) * c->P, cudaMemcpyDeviceToHost, st));
+    any = true;
+  }
+  if (ens_mean_logit) {
+    CK(c, cudaMemcpyAsync(ens_mean_logit, c->ens_logit, sizeof(float) * c->P, cudaMemcpyDeviceToHost, st));
+    any = true;
+  }
+  if (any) CK(c, cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {
+  if (!c || !c->member_logits) return HB_E_STATE;
+  if (ml) *ml = c->member_logits;
+  if (ep) *ep = c->ens_prob;
+  if (el) *el = c->ens_logit;
+  return HB_OK;
+}
+
+int hb_last_windows(hb_ctx* c, float* raw, float* stats, void* stream) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  cudaStream_t st = pick(c, stream);
+  const size_t S = static_cast<size_t>(c->P) * c->leads;
+  if (raw) {
+    if (!c->keep) return fail(c, HB_E_STATE, "context created without keep_windows");
+    CK(c, cudaMemcpyAsync(raw, c->raw, sizeof(float) * S * c->W, cudaMemcpyDeviceToHost, st));
+  }
+  if (stats) CK(c, cudaMemcpyAsync(stats, c->stats, sizeof(float) * S * 2, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+int hb_tick_work(const hb_ctx* c, double* flops, double* bytes) {
+  if (!c) return HB_E_INVALID;
+  double f = 0, b = 0;
+  for (int idx : c->selected) {
+    const Member& m = c->members.at(idx);
+    f += m.flops;
+    b += m.bytes;
+  }
+  if (flops) *flops = f * c->P;
+  if (bytes) *bytes = b * c->P;
+  return HB_OK;
+}
+
+// ----------------------------------------------------------------- test entry points
+
+int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
+                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, const float* fc_w_host,
+                 float* head_out, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int lout = (lin + stride - 1) / stride;
+  const int tot = (lout - 1) * stride + kTaps - lin;
+  const int pad = tot > 0 ? tot / 2 : 0;
+  const size_t wb = wpack_bytes(cin, cout);
+  std::vector<uint16_t> img(wb / 2);
+  pack_weights(w_host, cin, cout, stride, img.data());
+  const int bn = conv_bn(cout);
+  const int nbias = ((round_up(cout, 16) + bn - 1) / bn) * bn;
+  std::vector<float> bias(nbias, 0.f);
+  std::copy(b_host, b_host + cout, bias.begin());
+  uint8_t* dw = nullptr;
+  float *db = nullptr, *dfc = nullptr;
+  hb_ctx* none = nullptr;
+  CK(none, cudaMalloc(&dw, wb));
+  CK(none, cudaMemcpy(dw, img.data(), wb, cudaMemcpyHostToDevice));
+  CK(none, cudaMalloc(&db, sizeof(float) * nbias));
+  CK(none, cudaMemcpy(db, bias.data(), sizeof(float) * nbias, cudaMemcpyHostToDevice));
+  if (fc_w_host) {
+    CK(none, cudaMalloc(&dfc, sizeof(float) * cout));
+    CK(none, cudaMemcpy(dfc, fc_w_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
+  }
+  ConvPlan plan;
+  const int res_lp = round_up(res_len > 0 ? res_len : lout, 8);
+  const char* e = plan_conv(&plan, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
+                            round_up(lin, 8), static_cast<__half*>(out), dw, db, static_cast<const __half*>(res),
+                            res_mode, res_c, res_lp, dfc, head_out, sms);
+  int rc = HB_OK;
+  if (e) {
+    g_create_err = e;
+    rc = HB_E_INVALID;
+  } else {
+    cudaError_t ce = launch_conv(plan, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) {
+      g_create_err = std::string("conv launch: ") + cudaGetErrorString(ce);
+      rc = HB_E_CUDA;
+    }
+  }
+  cudaFree(dw);
+  cudaFree(db);
+  cudaFree(dfc);
+  return rc;
+}
+
+int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
+               void* stream) {
+  if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int tot = kTaps - 1;
+  float *dw = nullptr, *db = nullptr;
+  hb_ctx* none = nullptr;
+  CK(none, cudaMalloc(&dw, sizeof(float) * cout * kTaps));
+  CK(none, cudaMemcpy(dw, w_host, sizeof(float) * cout * kTaps, cudaMemcpyHostToDevice));
+  CK(none, cudaMalloc(&db, sizeof(float) * cout));
+  CK(none, cudaMemcpy(db, b_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
+  cudaError_t ce = launch_stem(static_cast<const __half*>(xn), L, P, L, round_up(L, 8), cout, tot / 2, dw, db,
+                               static_cast<__half*>(out), st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  cudaFree(dw);
+  cudaFree(db);
+  if (ce != cudaSuccess) return fail(none, HB_E_CUDA, cudaGetErrorString(ce));
+  return HB_OK;
+}
+
+int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
+                 int S, double* auc_out) {
+  (void)device; (void)scores; (void)labels; (void)N; (void)n; (void)selectors; (void)S; (void)auc_out;
+  return fail(nullptr, HB_E_STATE, "hb_sweep_auc: not built yet");
+}
+
+}  // extern "C"

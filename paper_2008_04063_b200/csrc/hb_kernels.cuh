@@ -1,0 +1,97 @@
+// Internal kernel interfaces shared by the C-ABI layer (hb_api.cu) and the
+// kernel translation units.  Activation layout everywhere ("NG8"):
+//   act[p][c/8][Lp][8]  fp16,  Lp = roundup(L, 8), rows [L, Lp) kept zero,
+// i.e. per patient, one contiguous [Lp x 16 B] plane per 8-channel group.  A
+// conv's implicit-GEMM A tile for one 8-channel group is then one contiguous
+// run of rows, and a tap shift is a 16-byte shift of the smem descriptor.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hb {
+
+constexpr int kTaps = 16;
+constexpr int kBM = 128;               // output positions per tile (UMMA M)
+constexpr int kConvThreads = 256;      // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-7 epilogue
+constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic smem on sm_100
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct ConvArgs {
+  int P, cin, cout, bn, n_ntiles;  // bn = per-tile N (mult of 16, <=256)
+  int lin, lout, lp_out;
+  int stride, pad, lo;             // lo: first A row (s=1) / pair (s=2) offset
+  int ck, n_kchunks, ksteps, rows; // channels per k-chunk, K-steps per chunk, A rows per parity
+  int mt_per_p, num_tiles;
+  uint32_t a_stage_bytes, b_chunk_bytes;
+  int na_stages, nb_slots, b_resident;
+  uint32_t tmem_cols;
+  const uint8_t* wpack;            // [ntile][kchunk][kstep][2][bn][16 B] fp16
+  const float* bias;               // [n_ntiles*bn] (zero padded)
+  __half* out;                     // NG8 [P][cout/8][lp_out][8]
+  const __half* res;               // shortcut source (NG8) or null
+  int res_mode;                    // 0 none, 1 identity, 2 maxpool(2)
+  int res_c, lp_res;
+  int relu;
+  const float* fc_w;               // head: [cout] -> head_out[P][mt_per_p] (null = no head)
+  float* head_out;
+};
+
+struct ConvPlan {
+  ConvArgs args;
+  CUtensorMap tmap;                // A operand view of the input activation
+  int grid;
+  uint32_t smem_bytes;
+};
+
+// Build a plan (tensor map + tiling) for one conv layer.  Returns 0 or an error string.
+const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lout, int stride, int pad,
+                      const __half* in, int lp_in, __half* out, const uint8_t* wpack, const float* bias,
+                      const __half* res, int res_mode, int res_c, int lp_res, const float* fc_w,
+                      float* head_out, int num_sms);
+// Host-side packing of canonical weights W[cout][cin][16] into the plan's B image.
+size_t wpack_bytes(int cin, int cout);
+void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */);
+int conv_bn(int cout);
+cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st);
+// one-time kernel attribute setup (opt-in shared memory); call before capture.
+cudaError_t init_conv_kernel();
+cudaError_t init_stream_kernels();
+inline cudaError_t init_kernels() {
+  cudaError_t e = init_conv_kernel();
+  return e != cudaSuccess ? e : init_stream_kernels();
+}
+
+// stem conv (C_in = 1) + bias + ReLU on CUDA cores: xn[p][L] fp16 -> NG8 out.
+cudaError_t launch_stem(const __half* xn, int x_stride, int P, int L, int lp_out, int cout, int pad,
+                        const float* w /*[cout][16]*/, const float* b, __half* out, cudaStream_t st);
+
+// K1+K2: ring append of `n_new` samples per stream at the device write cursor
+// *wpos, then (if xn != null) gather of the window ending at *wpos + n_new and
+// z-normalisation -> xn[lead][P][window] fp16.  raw_out (optional) receives the
+// raw gathered window [P][leads][window] fp32, stats (optional) mean/std.
+cudaError_t launch_ingest_window(const float* staged /*[P][leads][n_new]*/, float* ring /*[P][leads][R]*/,
+                                 const long long* wpos, int P, int leads, int n_new, int R, int window,
+                                 __half* xn, float* raw_out, float* stats, cudaStream_t st);
+cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st);
+
+// head + ensemble aggregation: partial[m][P][mt] -> member logits, ensemble outputs.
+struct HeadMember {
+  const float* partial;  // [P][mt]
+  int mt;
+  float inv_len;
+  float fc_b;
+};
+cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits /*[P][M]*/,
+                             float* ens_prob, float* ens_logit, cudaStream_t st);
+constexpr int kMaxMembers = 64;
+
+// profiler sweep (K6): exact midrank AUC of every selector's ensemble mean.
+cudaError_t launch_sweep_auc(const double* scores /*[N][n] row-major*/, const int8_t* labels, int N, int n,
+                             const uint32_t* selectors /*[S] bitmasks*/, int S, double* auc_out,
+                             void* scratch, size_t scratch_bytes, cudaStream_t st);
+size_t sweep_scratch_bytes(int N, int S);
+
+}  // namespace hb

@@ -1,0 +1,196 @@
+// K1/K2 (ring append, window gather, z-normalisation), K3 (stem conv on CUDA
+// cores) and K5 (head + ensemble aggregation).  All memory-bound or tiny.
+//
+// Reference counterparts (behaviour, not code):
+//   K1/K2 replace `Aggregator.add` buffering + `WindowBatch` materialisation
+//         (`pkg/src/zooserve/runtime.py:76-115`): at hop == window the gathered
+//         window k is exactly samples [k*W, (k+1)*W) of the stream.
+//   K5    replaces `_WindowScorer.draw`'s mean latent (`runtime.py:131-136`)
+//         and `ensemble_scores` (`cohort.py:89-97`): mean over the selected
+//         members in zoo order, normalised by popcount; it also emits the mean
+//         of member sigmoids (north star).  Fixed order, no float atomics.
+#include "hb_kernels.cuh"
+
+#include <cstdint>
+
+namespace hb {
+
+constexpr int kWinThreads = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];  // fixed order
+    red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// One CTA per (patient, lead) stream.
+__global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float* __restrict__ staged,
+                                                                    float* __restrict__ ring,
+                                                                    const long long* __restrict__ wpos_p, int P,
+                                                                    int leads, int n_new, int R, int W,
+                                                                    __half* __restrict__ xn,
+                                                                    float* __restrict__ raw_out,
+                                                                    float* __restrict__ stats) {
+  extern __shared__ float win[];  // [W] when gathering
+  __shared__ float red[33];
+  const int s = blockIdx.x;  // stream = p*leads + lead
+  const int p = s / leads, lead = s % leads;
+  const long long wpos = *wpos_p;
+  float* rs = ring + static_cast<size_t>(s) * R;
+  const float* src = staged + static_cast<size_t>(s) * n_new;
+  for (int i = threadIdx.x; i < n_new; i += blockDim.x) rs[(wpos + i) % R] = src[i];
+  if (xn == nullptr) return;
+  __syncthreads();
+  // window = samples [end - W, end) with end = wpos + n_new
+  const long long start = wpos + n_new - W;
+  float part = 0.f;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    const long long n = start + i;
+    const float v = (n >= 0) ? rs[n % R] : 0.f;
+    win[i] = v;
+    part += v;
+  }
+  const float mean = block_sum(part, red) / static_cast<float>(W);
+  float sq = 0.f;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    const float d = win[i] - mean;
+    sq += d * d;
+  }
+  const float var = block_sum(sq, red) / static_cast<float>(W);
+  const float sd = sqrtf(var);
+  const float rstd = 1.f / fmaxf(sd, 1e-6f);
+  __half* dst = xn + (static_cast<size_t>(lead) * P + p) * W;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) dst[i] = __float2half_rn((win[i] - mean) * rstd);
+  if (raw_out) {
+    float* r = raw_out + static_cast<size_t>(s) * W;
+    for (int i = threadIdx.x; i < W; i += blockDim.x) r[i] = win[i];
+  }
+  if (stats && threadIdx.x == 0) {
+    stats[2 * s] = mean;
+    stats[2 * s + 1] = sd;
+  }
+}
+
+__global__ void advance_kernel(long long* wpos, int n) { *wpos += n; }
+
+cudaError_t launch_ingest_window(const float* staged, float* ring, const long long* wpos, int P, int leads,
+                                 int n_new, int R, int window, __half* xn, float* raw_out, float* stats,
+                                 cudaStream_t st) {
+  const size_t smem = xn ? static_cast<size_t>(window) * sizeof(float) : 0;
+  ingest_window_kernel<<<P * leads, kWinThreads, smem, st>>>(staged, ring, wpos, P, leads, n_new, R, window, xn,
+                                                             raw_out, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t init_stream_kernels() {
+  return cudaFuncSetAttribute(ingest_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st) {
+  advance_kernel<<<1, 1, 0, st>>>(wpos, n);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K3 stem
+// out[p][g][l][8] = ReLU(b + sum_t w[c][t] * x[p][l + t - pad]),  rows [L, Lp) = 0.
+constexpr int kStemTile = 256;
+__global__ void __launch_bounds__(kStemTile) stem_kernel(const __half* __restrict__ xn, int x_stride, int L,
+                                                         int lp_out, int cout, int pad,
+                                                         const float* __restrict__ w,
+                                                         const float* __restrict__ b, __half* __restrict__ out) {
+  __shared__ float sx[kStemTile + kTaps];
+  __shared__ float sw[128 * kTaps];
+  __shared__ float sb[128];
+  const int p = blockIdx.y;
+  const int l0 = blockIdx.x * kStemTile;
+  const __half* x = xn + static_cast<size_t>(p) * x_stride;
+  for (int i = threadIdx.x; i < kStemTile + kTaps; i += blockDim.x) {
+    const int pos = l0 + i - pad;
+    sx[i] = (pos >= 0 && pos < L) ? __half2float(x[pos]) : 0.f;
+  }
+  for (int i = threadIdx.x; i < cout * kTaps; i += blockDim.x) sw[i] = w[i];
+  for (int i = threadIdx.x; i < cout; i += blockDim.x) sb[i] = b[i];
+  __syncthreads();
+  const int l = l0 + threadIdx.x;
+  if (l >= lp_out) return;
+  float xv[kTaps];
+#pragma unroll
+  for (int t = 0; t < kTaps; ++t) xv[t] = sx[threadIdx.x + t];
+  const bool valid = l < L;
+  const int G = cout / 8;
+  for (int g = 0; g < G; ++g) {
+    uint4 pk;
+    __half2* o2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      float a0 = sb[g * 8 + j], a1 = sb[g * 8 + j + 1];
+#pragma unroll
+      for (int t = 0; t < kTaps; ++t) {
+        a0 = fmaf(sw[(g * 8 + j) * kTaps + t], xv[t], a0);
+        a1 = fmaf(sw[(g * 8 + j + 1) * kTaps + t], xv[t], a1);
+      }
+      o2[j / 2] = valid ? __floats2half2_rn(fmaxf(a0, 0.f), fmaxf(a1, 0.f)) : __floats2half2_rn(0.f, 0.f);
+    }
+    *reinterpret_cast<uint4*>(out + ((static_cast<size_t>(p) * G + g) * lp_out + l) * 8) = pk;
+  }
+}
+
+cudaError_t launch_stem(const __half* xn, int x_stride, int P, int L, int lp_out, int cout, int pad, const float* w,
+                        const float* b, __half* out, cudaStream_t st) {
+  if (cout > 128 || cout % 8) return cudaErrorInvalidValue;
+  dim3 grid((lp_out + kStemTile - 1) / kStemTile, P);
+  stem_kernel<<<grid, kStemTile, 0, st>>>(xn, x_stride, L, lp_out, cout, pad, w, b, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5 aggregate
+// One CTA per patient; warp w handles members w, w+8, ...; lanes sum the
+// member's per-tile head partials (fixed shuffle tree), then thread 0 combines
+// members in zoo order.
+__global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __restrict__ mem, int M, int P,
+                                                        float* __restrict__ member_logits,
+                                                        float* __restrict__ ens_prob,
+                                                        float* __restrict__ ens_logit) {
+  __shared__ float s_logit[kMaxMembers];
+  const int p = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int m = warp; m < M; m += 8) {
+    const HeadMember hm = mem[m];
+    float s = 0.f;
+    for (int i = lane; i < hm.mt; i += 32) s += hm.partial[static_cast<size_t>(p) * hm.mt + i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) s_logit[m] = hm.fc_b + s * hm.inv_len;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sp = 0.f, sl = 0.f;
+    for (int m = 0; m < M; ++m) {
+      const float lg = s_logit[m];
+      member_logits[static_cast<size_t>(p) * M + m] = lg;
+      sp += 1.f / (1.f + expf(-lg));
+      sl += lg;
+    }
+    ens_prob[p] = sp / static_cast<float>(M);
+    ens_logit[p] = sl / static_cast<float>(M);
+  }
+}
+
+cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits, float* ens_prob,
+                             float* ens_logit, cudaStream_t st) {
+  if (M < 1 || M > kMaxMembers) return cudaErrorInvalidValue;
+  aggregate_kernel<<<P, 256, 0, st>>>(members_dev, M, P, member_logits, ens_prob, ens_logit);
+  return cudaGetLastError();
+}
+
+}  // namespace hb
