@@ -104,6 +104,12 @@ int hb_device_outputs(const hb_ctx* ctx, float** member_logits, float** ens_prob
 /* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
  * (mean, std) [P][n_leads][2] of the most recent tick. */
 int hb_last_windows(hb_ctx* ctx, float* raw, float* stats, void* stream);
+/* Eagerly launch one tick kernel-by-kernel with a CUDA event after every
+ * launch (same kernels and order as the graph) and report, per launch: kind
+ * (0 ingest/window, 1 stem, 2 tcgen05 conv, 3 aggregate, 4 cursor advance),
+ * device milliseconds, algorithmic FLOPs and bytes.  Returns the number of
+ * launches (>= 0) or -status.  Advances the stream cursor like a tick. */
+int hb_profile_tick(hb_ctx* ctx, void* stream, int cap, int* kinds, float* ms, double* flops, double* bytes);
 /* Algorithmic work of one tick: conv FLOPs and activation bytes (all selected members). */
 int hb_tick_work(const hb_ctx* ctx, double* flops, double* bytes);
 

@@ -50,6 +50,8 @@ _SIGS = {
     "hb_tick_device": (C.c_int, [_P, _P]),
     "hb_device_outputs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "hb_last_windows": (C.c_int, [_P, _F, _F, _P]),
+    "hb_profile_tick": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int), _F, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]),
     "hb_tick_work": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hb_sweep_auc": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,
                                C.POINTER(C.c_uint32), C.c_int, C.POINTER(C.c_double)]),

@@ -45,6 +45,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [4] per-warp head partials
+  uint32_t* s_aoff = reinterpret_cast<uint32_t*>(s_head + 4);  // [ksteps] A descriptor offsets (16 B units)
+  uint32_t* s_boff = s_aoff + 64;                              // [ksteps] B descriptor offsets
+  float* s_bias = reinterpret_cast<float*>(s_boff + 64);       // [bn]
+  float* s_fc = s_bias + 256;                                  // [bn]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -66,6 +70,33 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
+  // Per-K-step smem descriptor offsets, so the single MMA-issuing thread does
+  // no index arithmetic in its loop.  K-step ks covers (tap t, channel groups
+  // g, g+1) for 16+-channel chunks, or taps (t, t+stride) of the one 8-channel
+  // group; the A region of tap t is the tile's input rows shifted by t rows.
+  if (threadIdx.x < a.ksteps) {
+    const int ks = threadIdx.x;
+    int t, g;
+    if (a.ck >= 16) {
+      const int per_tap = a.ck / 16;
+      t = ks / per_tap;
+      g = 2 * (ks % per_tap);
+    } else {
+      t = (a.stride == 1) ? 2 * ks : (ks / 2) * 4 + (ks % 2);
+      g = 0;
+    }
+    const int u = t - a.pad;
+    const int q = u - a.stride * floordiv(u, a.stride);
+    const int row0 = floordiv(u, a.stride) - a.lo;
+    const uint32_t region_bytes = static_cast<uint32_t>((a.ck / 8) * a.rows * 16);
+    s_aoff[ks] = (static_cast<uint32_t>(q) * region_bytes + static_cast<uint32_t>(g * a.rows * 16 + row0 * 16)) >> 4;
+    s_boff[ks] = static_cast<uint32_t>(ks * 2 * a.bn * 16) >> 4;
+  }
+  for (int i = threadIdx.x; i < a.bn; i += blockDim.x) {
+    const int co = i;  // bias / fc are indexed per n-tile below (n_ntiles > 1 reloads per tile)
+    s_bias[i] = a.bias[co];
+    s_fc[i] = a.fc_w ? a.fc_w[co < a.cout ? co : 0] : 0.f;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -123,8 +154,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
       const uint32_t idesc = make_idesc_f16(kBM, a.bn);
-      const int groups = a.ck / 8;
-      const uint32_t region_bytes = static_cast<uint32_t>(groups * a.rows * 16);
       const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
       const uint32_t b_lbo = static_cast<uint32_t>(a.bn * 16);
       int as = 0;
@@ -149,26 +178,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           mbar_wait(&b_full[slot], a.b_resident ? bres_phase : bph);
           mbar_wait(&a_full[as], aph);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + static_cast<size_t>(as) * a.a_stage_bytes);
-          const uint32_t b_base = smem_u32(sB + static_cast<size_t>(slot) * a.b_chunk_bytes);
+          const uint64_t adesc = make_desc(smem_u32(sA + static_cast<size_t>(as) * a.a_stage_bytes), a_lbo, 128);
+          const uint64_t bdesc = make_desc(smem_u32(sB + static_cast<size_t>(slot) * a.b_chunk_bytes), b_lbo, 128);
+#pragma unroll 4
           for (int ks = 0; ks < a.ksteps; ++ks) {
-            int t, g;
-            if (a.ck >= 16) {
-              const int per_tap = a.ck / 16;
-              t = ks / per_tap;
-              g = 2 * (ks % per_tap);
-            } else {  // 8 channels: pair taps (t, t+1) for s=1, (t, t+2) for s=2
-              t = (a.stride == 1) ? 2 * ks : (ks / 2) * 4 + (ks % 2);
-              g = 0;
-            }
-            const int u = t - a.pad;
-            const int q = u - a.stride * floordiv(u, a.stride);
-            const int row0 = floordiv(u, a.stride) - a.lo;
-            const uint32_t a_addr =
-                a_base + static_cast<uint32_t>(q) * region_bytes + static_cast<uint32_t>(g * a.rows * 16 + row0 * 16);
-            const uint32_t b_addr = b_base + static_cast<uint32_t>(ks * 2 * a.bn * 16);
-            mma_f16_ss(d_tmem, make_desc(a_addr, a_lbo, 128), make_desc(b_addr, b_lbo, 128), idesc,
-                       (kc | ks) != 0 ? 1u : 0u);
+            mma_f16_ss(d_tmem, adesc + s_aoff[ks], bdesc + s_boff[ks], idesc, (kc | ks) != 0 ? 1u : 0u);
           }
           mma_commit(&a_empty[as]);
           if (!a.b_resident) {
@@ -197,6 +211,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     int acc = 0;
     uint32_t accph = 0;
     const int out_groups = a.cout / 8;
+    const int res_groups = a.res_mode ? a.res_c / 8 : 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int nt = tile / tiles_per_nt;
       const int rem = tile % tiles_per_nt;
@@ -205,62 +220,91 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int l = mt * kBM + r;
       const bool valid = l < a.lout;
       const bool in_buf = l < a.lp_out;
+      const int g0 = nt * (a.bn / 8);
+      const int ng = min(a.bn / 8, out_groups - g0);
+      const __half* res_p = a.res_mode ? a.res + static_cast<size_t>(p) * res_groups * a.lp_res * 8 : nullptr;
+      // Shortcut rows are independent of the accumulator: fetch the first 8
+      // groups while the MMAs of this tile are still running.
+      uint4 rres[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        rres[j] = make_uint4(0u, 0u, 0u, 0u);
+        const int g = g0 + j;
+        if (j < ng && g < res_groups && valid) {
+          const __half* src = res_p + static_cast<size_t>(g) * a.lp_res * 8;
+          if (a.res_mode == 1) {
+            rres[j] = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(l) * 8));
+          } else {
+            const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l) * 8));
+            const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l + 1) * 8));
+            const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
+            const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
+            __half2* o = reinterpret_cast<__half2*>(&rres[j]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] = __hmax2(h0[k], h1[k]);
+          }
+        }
+      }
+      const float* bias_t = (a.n_ntiles == 1) ? s_bias : a.bias + static_cast<size_t>(nt) * a.bn;
       mbar_wait(&acc_full[acc], accph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
       float head = 0.f;
-      for (int c0 = 0; c0 < a.bn; c0 += 16) {
+#pragma unroll
+      for (int c16 = 0; c16 < 16; ++c16) {
+        if (c16 * 2 >= ng) break;
         float v[16];
-        tmem_ld16(taddr + static_cast<uint32_t>(c0), v);
+        tmem_ld16(taddr + static_cast<uint32_t>(c16 * 16), v);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int co = nt * a.bn + c0 + 8 * h;  // first channel of this 8-group
-          const int g = co / 8;
-          if (g >= out_groups) continue;
+          const int j = 2 * c16 + h;
+          if (j >= ng) break;
+          const int g = g0 + j;
           float y[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) y[j] = v[8 * h + j] + __ldg(&a.bias[co + j]);
-          if (a.res_mode != 0 && co < a.res_c && valid) {
-            const __half* src = a.res + (static_cast<size_t>(p) * (a.res_c / 8) + g) * a.lp_res * 8;
-            if (a.res_mode == 1) {
-              const uint4 rv = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(l) * 8));
-              const __half2* h2 = reinterpret_cast<const __half2*>(&rv);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float2 f = __half22float2(h2[j]);
-                y[2 * j] += f.x;
-                y[2 * j + 1] += f.y;
-              }
+          for (int k = 0; k < 8; ++k) y[k] = v[8 * h + k] + bias_t[8 * j + k];
+          if (g < res_groups && valid) {
+            uint4 rv;
+            if (j < 8) {
+              rv = rres[j < 8 ? j : 0];
             } else {
-              const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l) * 8));
-              const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l + 1) * 8));
-              const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
-              const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
+              const __half* src = res_p + static_cast<size_t>(g) * a.lp_res * 8;
+              if (a.res_mode == 1) {
+                rv = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(l) * 8));
+              } else {
+                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l) * 8));
+                const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l + 1) * 8));
+                const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
+                const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
+                __half2* o = reinterpret_cast<__half2*>(&rv);
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float2 f = __half22float2(__hmax2(h0[j], h1[j]));
-                y[2 * j] += f.x;
-                y[2 * j + 1] += f.y;
+                for (int k = 0; k < 4; ++k) o[k] = __hmax2(h0[k], h1[k]);
               }
+            }
+            const __half2* h2 = reinterpret_cast<const __half2*>(&rv);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __half22float2(h2[k]);
+              y[2 * k] += f.x;
+              y[2 * k + 1] += f.y;
             }
           }
           if (a.relu) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] = fmaxf(y[j], 0.f);
+            for (int k = 0; k < 8; ++k) y[k] = fmaxf(y[k], 0.f);
           }
           if (a.fc_w != nullptr) {
             if (valid) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) head = fmaf(y[j], __ldg(&a.fc_w[co + j]), head);
+              for (int k = 0; k < 8; ++k) head = fmaf(y[k], s_fc[8 * j + k], head);
             }
           } else if (in_buf) {
             uint4 pk;
             __half2* o2 = reinterpret_cast<__half2*>(&pk);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              o2[j] = valid ? __floats2half2_rn(y[2 * j], y[2 * j + 1]) : __floats2half2_rn(0.f, 0.f);
-            __half* dst = a.out + ((static_cast<size_t>(p) * out_groups + g) * a.lp_out + l) * 8;
-            *reinterpret_cast<uint4*>(dst) = pk;
+            for (int k = 0; k < 4; ++k)
+              o2[k] = valid ? __floats2half2_rn(y[2 * k], y[2 * k + 1]) : __floats2half2_rn(0.f, 0.f);
+            *reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(p) * out_groups + g) * a.lp_out + l) * 8) = pk;
           }
         }
       }
@@ -276,8 +320,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (lane == 0) s_head[wq] = head;
         named_bar_sync(1, 128);
         if (wq == 0 && lane == 0) {
-          const float s = ((s_head[0] + s_head[1]) + s_head[2]) + s_head[3];
-          a.head_out[static_cast<size_t>(p) * a.mt_per_p + mt] = s;  // n_ntiles == 1 enforced for heads
+          const float sum = ((s_head[0] + s_head[1]) + s_head[2]) + s_head[3];
+          a.head_out[static_cast<size_t>(p) * a.mt_per_p + mt] = sum;  // n_ntiles == 1 enforced for heads
         }
         named_bar_sync(1, 128);
       }
@@ -300,7 +344,7 @@ int conv_bn(int cout) {
   return round_up((c + nt - 1) / nt, 16);
 }
 
-constexpr uint32_t kFixedSmem = 1024 + 256;  // barriers + holder + head scratch + slack
+constexpr uint32_t kFixedSmem = 1024 + 256 + 512 + 2048;  // barriers, holder, head scratch, K-step tables, bias/fc
 
 // Channels per k-chunk.  Prefer the largest chunk whose whole-layer weights
 // stay resident in smem next to two A stages; otherwise the largest chunk that
@@ -314,7 +358,7 @@ static int pick_ck(int cin, int cout, int stride, int* resident) {
   const int cands[4] = {64, 32, 16, 8};
   if (nnt == 1) {
     for (int ck : cands) {
-      if (cin % ck) continue;
+      if (cin % ck || cin / ck > 32) continue;
       const uint32_t b_all = 32u * cin * bn;  // 16 taps * cin * bn * 2 B
       const uint32_t a_stage = static_cast<uint32_t>(stride * rows * ck * 2);
       if (b_all + 2 * a_stage <= budget) {

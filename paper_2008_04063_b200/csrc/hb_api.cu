@@ -129,21 +129,53 @@ void free_member(Member& m) {
   cudaFree(m.head_partial);
 }
 
+// Kernel kinds reported by hb_profile_tick.
+enum { K_INGEST = 0, K_STEM = 1, K_CONV = 2, K_AGG = 3, K_ADV = 4 };
+
+struct ProfRec {
+  std::vector<cudaEvent_t>* ev = nullptr;  // event recorded after every launch
+  std::vector<int> kind;
+  std::vector<double> flops, bytes;
+  void mark(cudaStream_t st, int k, double f, double b) {
+    if (!ev) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev->push_back(e);
+    kind.push_back(k);
+    flops.push_back(f);
+    bytes.push_back(b);
+  }
+};
+
 // Enqueue the whole tick (after staging) on stream st.
-int enqueue_tick(hb_ctx* c, cudaStream_t st) {
+int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
+  ProfRec none;
+  if (!pr) pr = &none;
+  const double P = c->P;
   CK(c, launch_ingest_window(c->staged, c->ring, c->wpos, c->P, c->leads, c->hop, c->R, c->W, c->xn,
                              c->keep ? c->raw : nullptr, c->stats, st));
+  pr->mark(st, K_INGEST, 0.0, P * c->leads * (c->hop * 8.0 + c->W * 6.0));
   size_t pi = 0;
   for (int idx : c->selected) {
     Member& m = c->members[idx];
     const LayerSpec& s0 = m.layers[0];
     CK(c, launch_stem(c->xn + static_cast<size_t>(m.lead) * c->P * c->W, c->W, c->P, c->W,
                       round_up(s0.lout, 8), s0.cout, s0.pad, m.stem_w, m.stem_b, c->act[0], st));
-    for (size_t li = 1; li < m.layers.size(); ++li) CK(c, launch_conv(c->plans[pi++], st));
+    pr->mark(st, K_STEM, P * 2.0 * s0.cout * kTaps * s0.lout, P * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+    for (size_t li = 1; li < m.layers.size(); ++li) {
+      const LayerSpec& L = m.layers[li];
+      CK(c, launch_conv(c->plans[pi++], st));
+      pr->mark(st, K_CONV, P * 2.0 * L.cin * L.cout * kTaps * L.lout,
+               P * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
+                          (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
+    }
   }
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
                          c->ens_logit, st));
+  pr->mark(st, K_AGG, 0.0, 0.0);
   CK(c, launch_advance(c->wpos, c->hop, st));
+  pr->mark(st, K_ADV, 0.0, 0.0);
   return HB_OK;
 }
 
@@ -440,6 +472,39 @@ int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_pr
   }
   if (any) CK(c, cudaStreamSynchronize(st));
   return HB_OK;
+}
+
+int hb_profile_tick(hb_ctx* c, void* stream, int cap, int* kinds, float* ms, double* flops, double* bytes) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  const int rc0 = build_selection(c);
+  if (rc0) return rc0;
+  cudaStream_t st = pick(c, stream);
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t start;
+  CK(c, cudaEventCreate(&start));
+  CK(c, cudaEventRecord(start, st));
+  ProfRec pr;
+  pr.ev = &ev;
+  const int rc = enqueue_tick(c, st, &pr);
+  CK(c, cudaStreamSynchronize(st));
+  const int n = static_cast<int>(ev.size());
+  cudaEvent_t prev = start;
+  for (int i = 0; i < n; ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, prev, ev[i]);
+    if (i < cap) {
+      if (kinds) kinds[i] = pr.kind[i];
+      if (ms) ms[i] = t;
+      if (flops) flops[i] = pr.flops[i];
+      if (bytes) bytes[i] = pr.bytes[i];
+    }
+    prev = ev[i];
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(start);
+  if (rc) return rc;
+  return n;
 }
 
 int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {

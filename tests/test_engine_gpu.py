@@ -1,0 +1,113 @@
+"""End-to-end tick parity: ring ingest -> window -> z-norm -> every member's
+forward -> aggregation, on the device through the C-ABI, against the CPU oracle
+on identical synthetic streams.
+
+Bars (BASELINE.json north_star):
+  * window contents / indices: bit-exact (raw fp32 samples);
+  * member and ensemble probabilities: |dev - oracle| <= 1e-3 absolute;
+  * logits are compared too (sigmoid saturation cannot hide errors): <= 2e-2.
+"""
+import numpy as np
+import pytest
+
+from oracle import cnn, windows
+from paper_2008_04063_b200 import arch, synth
+from paper_2008_04063_b200.zoo import Selector, holmes_zoo
+
+pytestmark = pytest.mark.gpu
+
+PROB_TOL = 1e-3
+LOGIT_TOL = 2e-2
+C2 = [10, 13, 30, 50]   # ecg-i-w32-d8, ecg-i-w64-d4, ecg-ii-w32-d8, ecg-iii-w32-d8
+
+
+def _streams(P, n, seed=0, zero_patient=None):
+    s = synth.ecg_block(seed, P, 3, 0, n)
+    if zero_patient is not None:
+        s[zero_patient] = 0.0
+    return s
+
+
+def _oracle_tick(zoo, sel, streams, end, W=7500, seed=0):
+    P = streams.shape[0]
+    logits = []
+    for i in sel.indices():
+        prof = zoo.profiles[i]
+        win = np.stack([windows.sliding_window(streams[p, prof.lead], end, W) for p in range(P)])
+        params = arch.member_params(prof.width, prof.depth, seed, prof.id)
+        logits.append(cnn.member_forward(cnn.znorm(win), params, prof.width, prof.depth))
+    ml = np.stack(logits, axis=1)
+    prob, mean_logit = cnn.ensemble(ml)
+    return ml, prob, mean_logit
+
+
+def _compare(res, ml, prob, mean_logit):
+    assert np.abs(res.member_logits - ml).max() <= LOGIT_TOL, np.abs(res.member_logits - ml).max()
+    assert np.abs(cnn.sigmoid(res.member_logits) - cnn.sigmoid(ml)).max() <= PROB_TOL
+    assert np.abs(res.ens_prob - prob).max() <= PROB_TOL
+    assert np.abs(res.ens_mean_logit - mean_logit).max() <= LOGIT_TOL
+
+
+def test_sliding_ticks_match_oracle():
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, C2)
+    P, W, hop = 5, 7500, 250
+    streams = _streams(P, W + 2 * hop, zero_patient=3)
+    with EnsembleEngine(zoo, sel, P, hop=hop, keep_windows=True) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        for k in range(3):
+            end = W + k * hop
+            res = eng.tick(streams[:, :, end - hop:end])
+            raw, stats = eng.last_windows()
+            for p in range(P):
+                for lead in range(3):
+                    exp = windows.sliding_window(streams[p, lead], end, W)
+                    assert np.array_equal(raw[p, lead], exp), (k, p, lead)
+            assert np.all(stats[3, :, 1] == 0.0)          # constant stream: zero-variance guard
+            _compare(res, *_oracle_tick(zoo, sel, streams, end))
+
+
+def test_tumbling_mode_equals_aggregator_windows():
+    """hop == window: tick k scores exactly reference window k = samples [kW, (k+1)W)."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [10])
+    P, W = 2, 7500
+    streams = _streams(P, 2 * W, seed=3)
+    with EnsembleEngine(zoo, sel, P, hop=W, keep_windows=True) as eng:
+        for k in range(2):
+            res = eng.tick(streams[:, :, k * W:(k + 1) * W])
+            raw, _ = eng.last_windows()
+            for p in range(P):
+                for lead in range(3):
+                    tumbling = windows.tumbling_windows(streams[p, lead], W)
+                    assert np.array_equal(raw[p, lead], tumbling[k][1])
+            _compare(res, *_oracle_tick(zoo, sel, streams, (k + 1) * W))
+
+
+def test_selector_change_and_single_member():
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    P, W, hop = 3, 7500, 250
+    streams = _streams(P, W, seed=7)
+    sel_a = Selector.from_indices(60, [0, 21])      # w8-d2 lead I, w8-d4 lead II
+    with EnsembleEngine(zoo, sel_a, P, hop=hop) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        res = eng.tick(streams[:, :, W - hop:])
+        _compare(res, *_oracle_tick(zoo, sel_a, streams, W))
+        sel_b = Selector.from_indices(60, [6])       # ecg-i-w16-d16 (deep, 8 downsamples)
+        eng.set_selector(sel_b)
+        eng.ingest(np.zeros((P, 3, 0), np.float32))
+        # re-score the same window: rewind is not supported, so compare the next tick
+        more = synth.ecg_block(7, P, 3, W, hop)
+        full = np.concatenate([streams, more], axis=2)
+        res = eng.tick(more)
+        _compare(res, *_oracle_tick(zoo, sel_b, full, W + hop))
+
+
+def test_empty_selector_rejected():
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    from paper_2008_04063_b200.errors import EmptyEnsembleError
+    with pytest.raises(EmptyEnsembleError):
+        EnsembleEngine(holmes_zoo(), Selector.zeros(60), 2)
