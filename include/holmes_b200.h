@@ -120,10 +120,17 @@ int hb_tick_work(const hb_ctx* ctx, double* flops, double* bytes);
 int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
                  int S, double* auc_out);
 
-/* Kernel-level entry points used by the parity tests (device pointers). */
+/* Kernel-level entry points used by the parity tests (device pointers).
+ * Activation layouts (fp16, 8-channel groups g, see hb_kernels.cuh):
+ *   I: [P][C/8][roundup(L,8)][8];  S: [P][C/8][2][roundup(ceil(L/2),8)][8] (even/odd positions).
+ * A stride-1 conv reads I, a stride-2 conv reads S; res is I for res_mode 1
+ * (identity), S for res_mode 2 (maxpool(2) of a res_len-long block input);
+ * out_split selects the output layout. */
 int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
-                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, const float* fc_w_host,
-                 float* head_out, void* stream);
+                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
+                 const float* fc_w_host, float* head_out, void* stream);
+/* Micro-benchmark of one conv layer shape on zero data: mean ms per launch. */
+int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out);
 int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
                void* stream);
 

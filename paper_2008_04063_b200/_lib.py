@@ -56,7 +56,8 @@ _SIGS = {
     "hb_sweep_auc": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,
                                C.POINTER(C.c_uint32), C.c_int, C.POINTER(C.c_double)]),
     "hb_op_conv1d": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
-                               C.c_int, _P, _F, _P, _P]),
+                               C.c_int, _P, C.c_int, _F, _P, _P]),
+    "hb_bench_conv": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
     "hb_op_stem": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, _P]),
 }
 

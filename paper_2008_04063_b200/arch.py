@@ -100,7 +100,7 @@ def _fp16_round(a: np.ndarray) -> np.ndarray:
     return a.astype(np.float16).astype(np.float32)
 
 
-def _calibration_windows(n: int = 4, length: int = 1500) -> np.ndarray:
+def _calibration_windows(n: int = 8, length: int = 1500) -> np.ndarray:
     """Fixed z-normalised synthetic ECG used only to set BN statistics."""
     from .synth import ecg_samples
     x = np.stack([ecg_samples(12345, p, p % 3, 0, length) for p in range(n)]).astype(np.float64)
@@ -117,8 +117,9 @@ def member_params(width: int, depth: int, seed: int, member_id: str,
     batch (CPU, at parameter-synthesis time only — never on the scoring path)
     sets each channel's mean/var, then (gamma, beta) are drawn and folded into
     (W, b); folded W is rounded to fp16-representable values.  The residual
-    branch gain is 0.5.  The FC is scaled/centred on the calibration batch so
-    logits are O(1) and input dependent (sigmoid unsaturated).
+    branch gain is 0.5.  The FC is the top principal direction of the pooled
+    calibration features, scaled/centred so logits are O(1) and input
+    dependent (sigmoid unsaturated) without amplifying rounding noise.
     Returns {layer name: (W[cout, cin, 16] fp32, b[cout] fp32)} + "fc": (w, b[1]).
     """
     import torch
@@ -161,10 +162,15 @@ def member_params(width: int, depth: int, seed: int, member_id: str,
                 block_in = h
             h = torch.relu(y)
         pooled = h.mean(dim=-1).numpy().astype(np.float64)
-    c_last = specs[-1].cout
-    fc_w = rng.standard_normal(c_last)
+    # Head direction: the top principal component of the pooled features over
+    # the calibration batch (random sign), scaled so logits have std ~1.5.  A
+    # random direction would only see ~1/C of the input-dependent variance and
+    # the rescale would amplify fp16 rounding noise by ~sqrt(C).
+    centred = pooled - pooled.mean(axis=0, keepdims=True)
+    _, _, vt = np.linalg.svd(centred, full_matrices=False)
+    fc_w = vt[0] * (1.0 if rng.uniform() < 0.5 else -1.0)
     raw = pooled @ fc_w
-    fc_w *= 1.5 / max(raw.std(), 1e-3 * max(np.abs(raw).max(), 1e-6))
+    fc_w = fc_w * (1.5 / max(raw.std(), 1e-6))
     fc_b = -(pooled @ fc_w).mean() + rng.uniform(-0.5, 0.5)
     out["fc"] = (fc_w.astype(np.float32), np.array([fc_b], dtype=np.float32))
     return out

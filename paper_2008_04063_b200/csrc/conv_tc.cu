@@ -4,32 +4,45 @@
 //
 //   GEMM view (one tile = 128 output positions of one patient x bn channels):
 //     D[m, n] = sum_{t, c} X[s*(l0+m) + t - pad, c] * W[n, c, t]
-//   A (positions x K) is never materialised: the producer TMA-loads, per
-//   8-channel group, the contiguous run of input rows the tile touches (rows
-//   [l0-pad, l0-pad+144) for s=1; for s=2 the even and odd positions as two
-//   regions via a 5-D (pair, parity) tensor-map view).  The smem layout is the
-//   canonical K-major no-swizzle UMMA layout with rows 16 B apart, so tap t is
-//   the same region shifted by t rows: descriptor start + 16*t.  Out-of-range
-//   rows (the "same" padding) are zero-filled by TMA.
+//   A (positions x K) is never materialised.  Per 8-channel group the producer
+//   TMA-loads the contiguous run of input rows the tile touches as 128-byte
+//   lines (8 rows x 8 channels): rows [l0+row0, l0+row0+152) for s=1; for s=2
+//   the even- and odd-position planes of the parity-split (S) layout, 144 rows
+//   each.  That smem image is the canonical K-major no-swizzle UMMA layout
+//   (rows 16 B apart, SBO = 128 B), so tap t is the same region shifted by
+//   whole rows: descriptor start + 16 B * row offset.  "Same" padding rows
+//   outside [0, L) are zero-filled by TMA (negative / past-the-end lines) or
+//   are the zero rows every producer writes past L.
 //   B (weights) is pre-packed on the host into the exact smem image and moved
 //   with plain bulk copies; it stays resident in smem across tiles when the
 //   whole layer's weights fit.
 //
 // Roles (256 threads, 1 CTA/SM, persistent over tiles):
-//   warp 0  : TMA producer (one elected lane)
-//   warp 1  : MMA issuer (one lane), double-buffered TMEM accumulators
+//   warp 0  : TMA producer (one lane)
+//   warp 1  : MMA issuer (warp-uniform loop, one elected lane issues),
+//             double-buffered TMEM accumulators
 //   warp 2  : TMEM allocator
 //   warps 4-7: epilogue, thread r <-> TMEM lane r <-> output position l0+r
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
-#include <cstring>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace hb {
 
-__device__ __forceinline__ int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+constexpr int kRowsS1 = 152;  // A rows per group for stride 1 (19 TMA lines)
+constexpr int kRowsS2 = 144;  // A rows per (parity, group) for stride 2 (18 lines)
+
+__host__ __device__ __forceinline__ int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+__device__ __forceinline__ size_t out_offset(const ConvArgs& a, int p, int g, int l) {
+  const size_t plane = static_cast<size_t>(p) * (a.cout / 8) + g;
+  if (!a.out_split) return (plane * a.out_lp + l) * 8;
+  return ((plane * 2 + (l & 1)) * a.out_lh + (l >> 1)) * 8;
+}
 
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ ConvArgs a) {
@@ -45,9 +58,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [4] per-warp head partials
-  uint32_t* s_aoff = reinterpret_cast<uint32_t*>(s_head + 4);  // [ksteps] A descriptor offsets (16 B units)
-  uint32_t* s_boff = s_aoff + 64;                              // [ksteps] B descriptor offsets
-  float* s_bias = reinterpret_cast<float*>(s_boff + 64);       // [bn]
+  float* s_bias = s_head + 4;                                  // [bn]
   float* s_fc = s_bias + 256;                                  // [bn]
 
   const uint32_t warp = warp_id();
@@ -70,32 +81,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
-  // Per-K-step smem descriptor offsets, so the single MMA-issuing thread does
-  // no index arithmetic in its loop.  K-step ks covers (tap t, channel groups
-  // g, g+1) for 16+-channel chunks, or taps (t, t+stride) of the one 8-channel
-  // group; the A region of tap t is the tile's input rows shifted by t rows.
-  if (threadIdx.x < a.ksteps) {
-    const int ks = threadIdx.x;
-    int t, g;
-    if (a.ck >= 16) {
-      const int per_tap = a.ck / 16;
-      t = ks / per_tap;
-      g = 2 * (ks % per_tap);
-    } else {
-      t = (a.stride == 1) ? 2 * ks : (ks / 2) * 4 + (ks % 2);
-      g = 0;
-    }
-    const int u = t - a.pad;
-    const int q = u - a.stride * floordiv(u, a.stride);
-    const int row0 = floordiv(u, a.stride) - a.lo;
-    const uint32_t region_bytes = static_cast<uint32_t>((a.ck / 8) * a.rows * 16);
-    s_aoff[ks] = (static_cast<uint32_t>(q) * region_bytes + static_cast<uint32_t>(g * a.rows * 16 + row0 * 16)) >> 4;
-    s_boff[ks] = static_cast<uint32_t>(ks * 2 * a.bn * 16) >> 4;
-  }
   for (int i = threadIdx.x; i < a.bn; i += blockDim.x) {
-    const int co = i;  // bias / fc are indexed per n-tile below (n_ntiles > 1 reloads per tile)
-    s_bias[i] = a.bias[co];
-    s_fc[i] = a.fc_w ? a.fc_w[co < a.cout ? co : 0] : 0.f;
+    s_bias[i] = a.bias[i];
+    s_fc[i] = a.fc_w ? a.fc_w[i < a.cout ? i : 0] : 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -103,6 +91,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   const int tiles_per_nt = a.P * a.mt_per_p;
+  const int groups = a.ck / 8;
+  const uint32_t region_bytes = static_cast<uint32_t>(groups * a.rows * 16);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -112,13 +102,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       int bs = 0;
       uint32_t bph = 0;
       int loaded_nt = -1;
-      const int groups = a.ck / 8;
-      const uint32_t region_bytes = static_cast<uint32_t>(groups * a.rows * 16);
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
         const int nt = tile / tiles_per_nt;
         const int rem = tile % tiles_per_nt;
         const int p = rem / a.mt_per_p;
-        const int l0 = (rem % a.mt_per_p) * kBM;
+        const int blk = ((rem % a.mt_per_p) * kBM + a.row0) / 8;  // first 128-B line (8 rows)
         const bool load_b = !a.b_resident || nt != loaded_nt;
         loaded_nt = nt;
         for (int kc = 0; kc < a.n_kchunks; ++kc) {
@@ -138,10 +126,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           mbar_arrive_expect_tx(&a_full[as], a.a_stage_bytes);
           uint8_t* dst = sA + static_cast<size_t>(as) * a.a_stage_bytes;
           if (a.stride == 1) {
-            tma_load_4d(dst, &tmA, &a_full[as], 0, l0 + a.lo, kc * groups, p);
+            tma_load_4d(dst, &tmA, &a_full[as], 0, blk, kc * groups, p);
           } else {
-            tma_load_5d(dst, &tmA, &a_full[as], 0, 0, l0 + a.lo, kc * groups, p);
-            tma_load_5d(dst + region_bytes, &tmA, &a_full[as], 0, 1, l0 + a.lo, kc * groups, p);
+            tma_load_5d(dst, &tmA, &a_full[as], 0, blk, 0, kc * groups, p);
+            tma_load_5d(dst + region_bytes, &tmA, &a_full[as], 0, blk, 1, kc * groups, p);
           }
           if (++as == a.na_stages) {
             as = 0;
@@ -151,58 +139,135 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      const uint32_t idesc = make_idesc_f16(kBM, a.bn);
-      const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
-      const uint32_t b_lbo = static_cast<uint32_t>(a.bn * 16);
-      int as = 0;
-      uint32_t aph = 0;
-      int bs = 0;
-      uint32_t bph = 0;
-      int acc = 0;
-      uint32_t accph = 0;
-      int loaded_nt = -1;
-      uint32_t bres_phase = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-        const int nt = tile / tiles_per_nt;
-        if (a.b_resident && nt != loaded_nt) {
-          if (loaded_nt >= 0) bres_phase ^= 1;
-          loaded_nt = nt;
+    // -------------------------------------------------------------- MMA issuer
+    // The whole warp walks the loop with warp-uniform values (kept in uniform
+    // registers); one elected lane issues each tcgen05.mma / commit.
+    const uint32_t idesc = make_idesc_f16(kBM, a.bn);
+    const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
+    const uint32_t b_lbo = static_cast<uint32_t>(a.bn * 16);
+    const uint32_t rows16 = static_cast<uint32_t>(a.rows);  // one group column, 16 B units
+    const uint32_t region16 = region_bytes >> 4;           // one parity region
+    const uint32_t bstep16 = static_cast<uint32_t>(2 * a.bn);
+    const int per_tap = a.ck >> 4;  // 0 for 8-channel chunks
+    // stride-2 A offset (16 B units) of tap t in {0, 1}: parity region + pair row
+    auto toff_s2 = [&](int t) -> uint32_t {
+      const int u = t - a.pad;
+      return static_cast<uint32_t>(u & 1) * region16 + static_cast<uint32_t>((u >> 1) - a.row0);
+    };
+    int as = 0;
+    uint32_t aph = 0;
+    int bs = 0;
+    uint32_t bph = 0;
+    int acc = 0;
+    uint32_t accph = 0;
+    unsigned long long t_acc = 0, t_a = 0, t_issue = 0, t0 = 0;
+    const bool prof = (a.dbg & 8) && a.prof;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      if (prof) t0 = clock64();
+      mbar_wait(&acc_empty[acc], accph ^ 1);
+      if (prof) t_acc += clock64() - t0;
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bn);
+      for (int kc = 0; kc < a.n_kchunks; ++kc) {
+        const int slot = a.b_resident ? kc : bs;
+        if (prof) t0 = clock64();
+        mbar_wait(&b_full[slot], a.b_resident ? 0u : bph);
+        mbar_wait(&a_full[as], aph);
+        if (prof) {
+          const unsigned long long t1 = clock64();
+          t_a += t1 - t0;
+          t0 = t1;
         }
-        mbar_wait(&acc_empty[acc], accph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bn);
-        for (int kc = 0; kc < a.n_kchunks; ++kc) {
-          const int slot = a.b_resident ? kc : bs;
-          mbar_wait(&b_full[slot], a.b_resident ? bres_phase : bph);
-          mbar_wait(&a_full[as], aph);
-          tc_fence_after();
-          const uint64_t adesc = make_desc(smem_u32(sA + static_cast<size_t>(as) * a.a_stage_bytes), a_lbo, 128);
-          const uint64_t bdesc = make_desc(smem_u32(sB + static_cast<size_t>(slot) * a.b_chunk_bytes), b_lbo, 128);
-#pragma unroll 4
-          for (int ks = 0; ks < a.ksteps; ++ks) {
-            mma_f16_ss(d_tmem, adesc + s_aoff[ks], bdesc + s_boff[ks], idesc, (kc | ks) != 0 ? 1u : 0u);
-          }
-          mma_commit(&a_empty[as]);
-          if (!a.b_resident) {
-            mma_commit(&b_empty[bs]);
-            if (++bs == a.nb_slots) {
-              bs = 0;
-              bph ^= 1;
+        const uint64_t adesc = make_desc(smem_u32(sA + static_cast<size_t>(as) * a.a_stage_bytes), a_lbo, 128);
+        const uint64_t bdesc = make_desc(smem_u32(sB + static_cast<size_t>(slot) * a.b_chunk_bytes), b_lbo, 128);
+        // Descriptor walk with two 64-bit adds per MMA.  B K-steps are ordered
+        // (tap, 16-channel sub-chunk j); A for tap t is the region shifted by
+        // toff(t) rows: s=1 -> t - pad - row0 (+1 per tap); s=2 -> even/odd
+        // taps alternate parity regions, each advancing one row per tap pair.
+        uint32_t accum = kc > 0 ? 1u : 0u;
+        if (per_tap > 0) {
+          const uint32_t btap = static_cast<uint32_t>(per_tap) * bstep16;
+          for (int j = 0; j < per_tap; ++j) {
+            uint64_t bd = bdesc + static_cast<uint32_t>(j) * bstep16;
+            if (a.stride == 1) {
+              uint64_t ad = adesc + static_cast<uint32_t>(2 * j) * rows16 + static_cast<uint32_t>(-a.pad - a.row0);
+#pragma unroll
+              for (int t = 0; t < kTaps; ++t) {
+                if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+                accum = 1u;
+                ad += 1;
+                bd += btap;
+              }
+            } else {
+              const uint64_t ag = adesc + static_cast<uint32_t>(2 * j) * rows16;
+              uint64_t a0 = ag + toff_s2(0), a1 = ag + toff_s2(1);
+#pragma unroll
+              for (int tp = 0; tp < kTaps / 2; ++tp) {
+                if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+                accum = 1u;
+                bd += btap;
+                if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+                bd += btap;
+                a0 += 1;
+                a1 += 1;
+              }
             }
           }
-          if (++as == a.na_stages) {
-            as = 0;
-            aph ^= 1;
+        } else {
+          // 8-channel chunk: one K-step pairs taps (t, t+1) [s=1] or (t, t+2) [s=2],
+          // i.e. the same region one row apart (LBO = 16 B)
+          uint64_t bd = bdesc;
+          if (a.stride == 1) {
+            uint64_t ad = adesc + static_cast<uint32_t>(-a.pad - a.row0);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+              accum = 1u;
+              ad += 2;
+              bd += bstep16;
+            }
+          } else {
+            uint64_t a0 = adesc + toff_s2(0), a1 = adesc + toff_s2(1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+              accum = 1u;
+              bd += bstep16;
+              if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+              bd += bstep16;
+              a0 += 2;
+              a1 += 2;
+            }
           }
         }
-        mma_commit(&acc_full[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          accph ^= 1;
+        __syncwarp();
+        if (prof) t_issue += clock64() - t0;
+        if (elect_one()) {
+          mma_commit(&a_empty[as]);
+          if (!a.b_resident) mma_commit(&b_empty[bs]);
+        }
+        __syncwarp();
+        if (!a.b_resident && ++bs == a.nb_slots) {
+          bs = 0;
+          bph ^= 1;
+        }
+        if (++as == a.na_stages) {
+          as = 0;
+          aph ^= 1;
         }
       }
+      if (elect_one()) mma_commit(&acc_full[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        accph ^= 1;
+      }
+    }
+    if (prof && lane == 0) {
+      a.prof[blockIdx.x * 8 + 0] = t_acc;
+      a.prof[blockIdx.x * 8 + 1] = t_a;
+      a.prof[blockIdx.x * 8 + 2] = t_issue;
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
@@ -212,6 +277,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint32_t accph = 0;
     const int out_groups = a.cout / 8;
     const int res_groups = a.res_mode ? a.res_c / 8 : 0;
+    const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0;
+    unsigned long long e_wait = 0, e_work = 0, et0 = 0, e_start = eprof ? clock64() : 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int nt = tile / tiles_per_nt;
       const int rem = tile % tiles_per_nt;
@@ -219,24 +286,25 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int mt = rem % a.mt_per_p;
       const int l = mt * kBM + r;
       const bool valid = l < a.lout;
-      const bool in_buf = l < a.lp_out;
+      const bool in_buf = l < a.out_rows;
       const int g0 = nt * (a.bn / 8);
       const int ng = min(a.bn / 8, out_groups - g0);
-      const __half* res_p = a.res_mode ? a.res + static_cast<size_t>(p) * res_groups * a.lp_res * 8 : nullptr;
       // Shortcut rows are independent of the accumulator: fetch the first 8
       // groups while the MMAs of this tile are still running.
+      // identity: block input in I layout; maxpool: block input in S layout,
+      // max(x[2l], x[2l+1]) = max(even plane row l, odd plane row l).
       uint4 rres[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         rres[j] = make_uint4(0u, 0u, 0u, 0u);
         const int g = g0 + j;
         if (j < ng && g < res_groups && valid) {
-          const __half* src = res_p + static_cast<size_t>(g) * a.lp_res * 8;
+          const size_t plane = static_cast<size_t>(p) * res_groups + g;
           if (a.res_mode == 1) {
-            rres[j] = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(l) * 8));
+            rres[j] = __ldg(reinterpret_cast<const uint4*>(a.res + (plane * a.res_rows + l) * 8));
           } else {
-            const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l) * 8));
-            const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l + 1) * 8));
+            const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2) * a.res_rows + l) * 8));
+            const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2 + 1) * a.res_rows + l) * 8));
             const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
             const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
             __half2* o = reinterpret_cast<__half2*>(&rres[j]);
@@ -246,7 +314,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
       }
       const float* bias_t = (a.n_ntiles == 1) ? s_bias : a.bias + static_cast<size_t>(nt) * a.bn;
+      if (eprof) et0 = clock64();
       mbar_wait(&acc_full[acc], accph);
+      if (eprof) {
+        const unsigned long long t1 = clock64();
+        e_wait += t1 - et0;
+        et0 = t1;
+      }
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
       float head = 0.f;
@@ -268,12 +342,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (j < 8) {
               rv = rres[j < 8 ? j : 0];
             } else {
-              const __half* src = res_p + static_cast<size_t>(g) * a.lp_res * 8;
+              const size_t plane = static_cast<size_t>(p) * res_groups + g;
               if (a.res_mode == 1) {
-                rv = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(l) * 8));
+                rv = __ldg(reinterpret_cast<const uint4*>(a.res + (plane * a.res_rows + l) * 8));
               } else {
-                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l) * 8));
-                const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(src + static_cast<size_t>(2 * l + 1) * 8));
+                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2) * a.res_rows + l) * 8));
+                const uint4 r1 =
+                    __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2 + 1) * a.res_rows + l) * 8));
                 const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
                 const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
                 __half2* o = reinterpret_cast<__half2*>(&rv);
@@ -304,12 +379,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               o2[k] = valid ? __floats2half2_rn(y[2 * k], y[2 * k + 1]) : __floats2half2_rn(0.f, 0.f);
-            *reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(p) * out_groups + g) * a.lp_out + l) * 8) = pk;
+            *reinterpret_cast<uint4*>(a.out + out_offset(a, p, g, l)) = pk;
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
+      if (eprof) e_work += clock64() - et0;
       if (++acc == 2) {
         acc = 0;
         accph ^= 1;
@@ -326,6 +402,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         named_bar_sync(1, 128);
       }
     }
+    if (eprof) {
+      a.prof[blockIdx.x * 8 + 3] = e_wait;
+      a.prof[blockIdx.x * 8 + 4] = e_work;
+      a.prof[blockIdx.x * 8 + 5] = clock64() - e_start;
+    }
   }
 
   tc_fence_before();
@@ -339,12 +420,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 int conv_bn(int cout) {
   const int c = round_up(cout < 16 ? 16 : cout, 16);
   if (c <= 256) return c;
-  // split N into equal tiles of <= 256 (multiple of 16)
-  const int nt = (c + 255) / 256;
+  const int nt = (c + 255) / 256;  // split N into equal tiles of <= 256 (multiple of 16)
   return round_up((c + nt - 1) / nt, 16);
 }
 
-constexpr uint32_t kFixedSmem = 1024 + 256 + 512 + 2048;  // barriers, holder, head scratch, K-step tables, bias/fc
+constexpr uint32_t kFixedSmem = 1024 + 256 + 2048;  // barriers, holder/head scratch, bias/fc
+
+static int a_rows(int stride) { return stride == 1 ? kRowsS1 : kRowsS2; }
 
 // Channels per k-chunk.  Prefer the largest chunk whose whole-layer weights
 // stay resident in smem next to two A stages; otherwise the largest chunk that
@@ -353,14 +435,13 @@ constexpr uint32_t kFixedSmem = 1024 + 256 + 512 + 2048;  // barriers, holder, h
 static int pick_ck(int cin, int cout, int stride, int* resident) {
   const int bn = conv_bn(cout);
   const int nnt = (round_up(cout, 16) + bn - 1) / bn;
-  const int rows = (stride == 1) ? kBM + 16 : kBM + 8;
   const uint32_t budget = kSmemLimit - kFixedSmem;
   const int cands[4] = {64, 32, 16, 8};
   if (nnt == 1) {
     for (int ck : cands) {
       if (cin % ck || cin / ck > 32) continue;
       const uint32_t b_all = 32u * cin * bn;  // 16 taps * cin * bn * 2 B
-      const uint32_t a_stage = static_cast<uint32_t>(stride * rows * ck * 2);
+      const uint32_t a_stage = static_cast<uint32_t>(stride * a_rows(stride) * ck * 2);
       if (b_all + 2 * a_stage <= budget) {
         *resident = 1;
         return ck;
@@ -370,7 +451,7 @@ static int pick_ck(int cin, int cout, int stride, int* resident) {
   for (int ck : cands) {
     if (cin % ck) continue;
     const uint32_t b_chunk = 32u * ck * bn;
-    const uint32_t a_stage = static_cast<uint32_t>(stride * rows * ck * 2);
+    const uint32_t a_stage = static_cast<uint32_t>(stride * a_rows(stride) * ck * 2);
     if (2 * b_chunk + 2 * a_stage <= budget) {
       *resident = 0;
       return ck;
@@ -386,12 +467,10 @@ size_t wpack_bytes(int cin, int cout) {
   return static_cast<size_t>(nnt) * bn * cin * kTaps * 2;
 }
 
-// B image per (ntile, kchunk): [kstep][half][bn rows][8 fp16], the K-step
-// order matching the MMA issuer (tap-major, then 16-channel sub-chunks; for
-// 8-channel chunks taps are paired (t,t+1) for s=1 or (t,t+2) for s=2 — the
-// pairing only depends on the consumer's stride, so a stride-specific image
-// is built: see pack_weights_strided).
-static void pack_weights_strided(const float* w, int cin, int cout, int stride, uint16_t* dst) {
+// B image per (ntile, kchunk): [kstep][half][bn rows][8 fp16] in the MMA
+// issuer's K-step order (tap-major, then 16-channel sub-chunks; 8-channel
+// chunks pair taps (t, t+1) for s=1 or (t, t+2) for s=2).
+void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) {
   const int bn = conv_bn(cout);
   const int nnt = (round_up(cout, 16) + bn - 1) / bn;
   int resident;
@@ -426,10 +505,6 @@ static void pack_weights_strided(const float* w, int cin, int cout, int stride, 
         }
 }
 
-void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) {
-  pack_weights_strided(w, cin, cout, stride, dst);
-}
-
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -447,13 +522,12 @@ static EncodeTiledFn get_encode() {
 }
 
 const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lout, int stride, int pad,
-                      const __half* in, int lp_in, __half* out, const uint8_t* wpack, const float* bias,
-                      const __half* res, int res_mode, int res_c, int lp_res, const float* fc_w,
+                      const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
+                      const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
                       float* head_out, int num_sms) {
   std::memset(plan, 0, sizeof(*plan));
   if (cin % 8 || cout % 8) return "conv: channels must be multiples of 8";
   if (stride != 1 && stride != 2) return "conv: stride must be 1 or 2";
-  if (stride == 2 && (lp_in % 2)) return "conv: stride-2 input needs even padded length";
   if (lout != (lin + stride - 1) / stride) return "conv: lout must be ceil(lin/stride)";
   ConvArgs& a = plan->args;
   a.P = P;
@@ -464,28 +538,38 @@ const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lou
   if (fc_w && a.n_ntiles != 1) return "conv: fused head needs cout <= 256";
   a.lin = lin;
   a.lout = lout;
-  a.lp_out = round_up(lout, 8);
+  a.out_split = out_split;
+  a.out_lp = lp_I(lout);
+  a.out_lh = lh_S(lout);
+  a.out_rows = fc_w ? lout : act_rows(lout, out_split);
   a.stride = stride;
   a.pad = pad;
-  a.lo = (stride == 1) ? -pad : -((pad + 1) / 2);  // floor(-pad/2)
+  a.rows = a_rows(stride);
+  if (stride == 1) {
+    a.row0 = -8 * ((pad + 7) / 8);
+    if (kBM - 1 + (kTaps - 1 - pad - a.row0) >= a.rows) return "conv: padding too large for the A tile";
+  } else {
+    a.row0 = 8 * floordiv(floordiv(-pad, 2), 8);
+    if (kBM - 1 + (floordiv(kTaps - 1 - pad, 2) - a.row0) >= a.rows) return "conv: padding too large for the A tile";
+  }
   int resident = 0;
   a.ck = pick_ck(cin, cout, stride, &resident);
   if (a.ck == 0) return "conv: no k-chunk fits in shared memory";
   a.n_kchunks = cin / a.ck;
-  a.ksteps = (a.ck >= 16) ? a.ck : 8;
-  a.rows = (stride == 1) ? kBM + 16 : kBM + 8;
-  a.mt_per_p = (lout + kBM - 1) / kBM;
+  const int ksteps = (a.ck >= 16) ? a.ck : 8;
+  a.mt_per_p = (a.out_rows + kBM - 1) / kBM;
   a.num_tiles = a.n_ntiles * P * a.mt_per_p;
   a.a_stage_bytes = static_cast<uint32_t>(stride * (a.ck / 8) * a.rows * 16);
-  a.b_chunk_bytes = static_cast<uint32_t>(a.ksteps * 2 * a.bn * 16);
-  const uint32_t fixed = kFixedSmem;
-  const uint32_t budget = kSmemLimit - fixed;
+  a.b_chunk_bytes = static_cast<uint32_t>(ksteps * 2 * a.bn * 16);
+  const uint32_t budget = kSmemLimit - kFixedSmem;
   const uint32_t b_all = a.b_chunk_bytes * a.n_kchunks;
   a.b_resident = resident;
   a.nb_slots = resident ? a.n_kchunks : 2;
   const uint32_t b_smem = resident ? b_all : 2 * a.b_chunk_bytes;
   a.na_stages = static_cast<int>((budget - b_smem) / a.a_stage_bytes);
-  if (a.na_stages > 4) a.na_stages = 4;
+  const int dbg = getenv("HB_DEBUG") ? atoi(getenv("HB_DEBUG")) : 0;
+  const int max_stages = (dbg & 2) ? 8 : (dbg & 4) ? 12 : 4;
+  if (a.na_stages > max_stages) a.na_stages = max_stages;
   if (a.na_stages < 2) return "conv: k-chunk does not fit in shared memory";
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(2 * a.bn)) cols <<= 1;
@@ -494,37 +578,37 @@ const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lou
   a.bias = bias;
   a.out = out;
   a.res = res;
-  a.res_mode = res_mode;
+  a.res_mode = res ? res_mode : 0;
   a.res_c = res_c;
-  a.lp_res = lp_res;
+  a.res_rows = (res_mode == 2) ? lh_S(res_len) : lp_I(res_len);
+  if (a.res && a.res_mode == 2 && lh_S(res_len) * 2 < 2 * lout) return "conv: maxpool shortcut shorter than the output";
   a.relu = 1;
   a.fc_w = fc_w;
   a.head_out = head_out;
-  plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + fixed;
+  a.dbg = dbg;
+  plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + kFixedSmem;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
 
   EncodeTiledFn enc = get_encode();
   if (!enc) return "conv: cuTensorMapEncodeTiled unavailable";
-  const int G = cin / 8;
+  const cuuint64_t G = static_cast<cuuint64_t>(cin / 8);
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult rc;
-  if (stride == 1) {
-    const cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(lp_in), static_cast<cuuint64_t>(G),
-                                static_cast<cuuint64_t>(P)};
-    const cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(lp_in) * 16,
-                                   static_cast<cuuint64_t>(G) * lp_in * 16};
-    const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(a.rows), static_cast<cuuint32_t>(a.ck / 8), 1};
+  if (stride == 1) {  // I layout: [P][G][lp][8] as {64 elems = 8 rows, lp/8 lines, G, P}
+    const cuuint64_t lp = static_cast<cuuint64_t>(lp_I(lin));
+    const cuuint64_t dims[4] = {64, lp / 8, G, static_cast<cuuint64_t>(P)};
+    const cuuint64_t strides[3] = {128, lp * 16, G * lp * 16};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(a.rows / 8), static_cast<cuuint32_t>(a.ck / 8), 1};
     rc = enc(&plan->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(in), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else {
-    const cuuint64_t dims[5] = {8, 2, static_cast<cuuint64_t>(lp_in / 2), static_cast<cuuint64_t>(G),
-                                static_cast<cuuint64_t>(P)};
-    const cuuint64_t strides[4] = {16, 32, static_cast<cuuint64_t>(lp_in) * 16,
-                                   static_cast<cuuint64_t>(G) * lp_in * 16};
-    const cuuint32_t box[5] = {8, 1, static_cast<cuuint32_t>(a.rows), static_cast<cuuint32_t>(a.ck / 8), 1};
+  } else {  // S layout: [P][G][2][lh][8] as {64, lh/8 lines, 2 parities, G, P}
+    const cuuint64_t lh = static_cast<cuuint64_t>(lh_S(lin));
+    const cuuint64_t dims[5] = {64, lh / 8, 2, G, static_cast<cuuint64_t>(P)};
+    const cuuint64_t strides[4] = {128, lh * 16, 2 * lh * 16, G * 2 * lh * 16};
+    const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(a.rows / 8), 1, static_cast<cuuint32_t>(a.ck / 8), 1};
     rc = enc(&plan->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(in), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (rc != CUDA_SUCCESS) return "conv: cuTensorMapEncodeTiled rejected the activation view";

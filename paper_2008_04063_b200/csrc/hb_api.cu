@@ -187,7 +187,7 @@ int build_selection(hb_ctx* c) {
   size_t need = 0;
   for (int idx : c->selected)
     for (auto& L : c->members[idx].layers)
-      need = std::max(need, static_cast<size_t>(c->P) * L.cout * round_up(L.lout, 8) * sizeof(__half));
+      need = std::max(need, static_cast<size_t>(c->P) * L.cout * act_rows(L.lout, 1) * sizeof(__half));
   for (auto& a : c->act) {
     CK(c, cudaMalloc(&a, need));
     CK(c, cudaMemset(a, 0, need));
@@ -201,24 +201,27 @@ int build_selection(hb_ctx* c) {
   for (int idx : c->selected) {
     Member& m = c->members[idx];
     int cur = 0;
+    const int nblocks = static_cast<int>(m.layers.size() - 1) / 2;
     for (size_t li = 1; li < m.layers.size(); ++li) {
       const LayerSpec& L = m.layers[li];
       const bool conv1 = (li % 2 == 1);
-      int src = cur, dst;
+      const int blk = static_cast<int>(li - 1) / 2;
+      int src = cur, dst, out_split = 0, res_len = 0;
       const __half* res = nullptr;
-      int res_lp = 0;
       if (conv1) {
         dst = (cur + 1) % 3;
       } else {
         src = (cur + 1) % 3;
         dst = (cur + 2) % 3;
         res = c->act[cur];
-        res_lp = round_up(m.layers[li - 1].lin, 8);
+        res_len = m.layers[li - 1].lin;
+        // the output of an even block feeds the next (stride-2) block: parity-split layout
+        out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
       }
       ConvPlan plan;
       const char* e = plan_conv(&plan, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, c->act[src],
-                                round_up(L.lin, 8), L.head ? nullptr : c->act[dst], m.wpack[li - 1], m.bias[li - 1],
-                                res, conv1 ? 0 : L.res_mode, L.res_c, res_lp, L.head ? m.fc_w : nullptr,
+                                L.head ? nullptr : c->act[dst], out_split, m.wpack[li - 1], m.bias[li - 1], res,
+                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? m.fc_w : nullptr,
                                 L.head ? m.head_partial : nullptr, c->num_sms);
       if (e) return fail(c, HB_E_INVALID, e);
       c->plans.push_back(plan);
@@ -545,8 +548,8 @@ int hb_tick_work(const hb_ctx* c, double* flops, double* bytes) {
 // ----------------------------------------------------------------- test entry points
 
 int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
-                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, const float* fc_w_host,
-                 float* head_out, void* stream) {
+                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
+                 const float* fc_w_host, float* head_out, void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
@@ -575,10 +578,9 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
     CK(none, cudaMemcpy(dfc, fc_w_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
   }
   ConvPlan plan;
-  const int res_lp = round_up(res_len > 0 ? res_len : lout, 8);
   const char* e = plan_conv(&plan, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
-                            round_up(lin, 8), static_cast<__half*>(out), dw, db, static_cast<const __half*>(res),
-                            res_mode, res_c, res_lp, dfc, head_out, sms);
+                            static_cast<__half*>(out), out_split, dw, db, static_cast<const __half*>(res), res_mode,
+                            res_c, res_len > 0 ? res_len : lout, dfc, head_out, sms);
   int rc = HB_OK;
   if (e) {
     g_create_err = e;
@@ -594,6 +596,87 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
   cudaFree(dw);
   cudaFree(db);
   cudaFree(dfc);
+  return rc;
+}
+
+int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int lout = (lin + stride - 1) / stride;
+  const int tot = (lout - 1) * stride + kTaps - lin;
+  const int pad = tot > 0 ? tot / 2 : 0;
+  const size_t in_b = static_cast<size_t>(P) * cin * act_rows(lin, 1) * 2;
+  const size_t out_b = static_cast<size_t>(P) * cout * act_rows(lout, 1) * 2;
+  const size_t wb = wpack_bytes(cin, cout);
+  const int bn = conv_bn(cout);
+  const int nbias = ((round_up(cout, 16) + bn - 1) / bn) * bn;
+  void *din = nullptr, *dout = nullptr, *dres = nullptr, *dw = nullptr, *db = nullptr;
+  hb_ctx* none = nullptr;
+  CK(none, cudaMalloc(&din, in_b));
+  CK(none, cudaMemset(din, 0, in_b));
+  CK(none, cudaMalloc(&dout, out_b));
+  CK(none, cudaMalloc(&dres, in_b > out_b ? in_b : out_b));
+  CK(none, cudaMemset(dres, 0, in_b > out_b ? in_b : out_b));
+  CK(none, cudaMalloc(&dw, wb));
+  CK(none, cudaMemset(dw, 0, wb));
+  CK(none, cudaMalloc(&db, nbias * 4));
+  CK(none, cudaMemset(db, 0, nbias * 4));
+  ConvPlan plan;
+  const char* e = plan_conv(&plan, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
+                            static_cast<__half*>(dout), 0, static_cast<uint8_t*>(dw), static_cast<float*>(db),
+                            res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
+                            res_mode == 2 ? 2 * lin : lout, nullptr, nullptr, sms);
+  int rc = HB_OK;
+  unsigned long long* dprof = nullptr;
+  if (!e && (plan.args.dbg & 8)) {
+    cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * plan.grid);
+    cudaMemset(dprof, 0, sizeof(unsigned long long) * 8 * plan.grid);
+    plan.args.prof = dprof;
+  }
+  if (e) {
+    g_create_err = e;
+    rc = HB_E_INVALID;
+  } else {
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int i = 0; i < 3; ++i) launch_conv(plan, st);
+    cudaEventRecord(a, st);
+    for (int i = 0; i < iters; ++i) launch_conv(plan, st);
+    cudaEventRecord(b, st);
+    cudaError_t ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    if (dprof) {
+      std::vector<unsigned long long> h(8 * plan.grid);
+      cudaMemcpy(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost);
+      double sum[8] = {0};
+      for (int i = 0; i < plan.grid; ++i)
+        for (int k = 0; k < 8; ++k) sum[k] += static_cast<double>(h[i * 8 + k]) / plan.grid;
+      const double tiles = static_cast<double>(plan.args.num_tiles) / plan.grid;
+      fprintf(stderr, "[prof] per tile (cycles): mma wait_acc %.0f wait_a %.0f issue %.0f | epi wait %.0f work %.0f | epi total/tile %.0f (tiles/CTA %.1f)\n",
+              sum[0] / tiles, sum[1] / tiles, sum[2] / tiles, sum[3] / tiles, sum[4] / tiles, sum[5] / tiles, tiles);
+      cudaFree(dprof);
+    }
+    if (ce != cudaSuccess) {
+      g_create_err = cudaGetErrorString(ce);
+      rc = HB_E_CUDA;
+    }
+  }
+  cudaFree(din);
+  cudaFree(dout);
+  cudaFree(dres);
+  cudaFree(dw);
+  cudaFree(db);
   return rc;
 }
 

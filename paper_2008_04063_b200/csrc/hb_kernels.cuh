@@ -19,24 +19,40 @@ constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic smem on sm_100
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// Activation layouts (fp16, per patient p and 8-channel group g of G):
+//   I  "interleaved":  rows l of a plane of lp_I(L) rows, element ((p*G+g)*lp + l)*8 + c
+//   S  "parity-split": two planes of lh_S(L) rows each (even / odd positions),
+//                      position l at (((p*G+g)*2 + (l&1))*lh + (l>>1))*8 + c
+// Padding rows (positions >= L inside the planes) are always written as zero
+// by the producing kernel.  A stride-1 conv reads I; a stride-2 conv reads S
+// (so that both parities are contiguous runs of 128-byte TMA lines); the conv
+// feeding a stride-2 conv writes S.
+inline int lp_I(int L) { return round_up(L, 8); }
+inline int lh_S(int L) { return round_up((L + 1) / 2, 8); }
+inline int act_rows(int L, int split) { return split ? 2 * lh_S(L) : lp_I(L); }
+
 struct ConvArgs {
   int P, cin, cout, bn, n_ntiles;  // bn = per-tile N (mult of 16, <=256)
-  int lin, lout, lp_out;
-  int stride, pad, lo;             // lo: first A row (s=1) / pair (s=2) offset
-  int ck, n_kchunks, ksteps, rows; // channels per k-chunk, K-steps per chunk, A rows per parity
+  int lin, lout;
+  int out_split, out_lp, out_lh;   // output layout (I: out_lp rows; S: 2 x out_lh rows)
+  int out_rows;                    // positions that must be written (valid or zero padding)
+  int stride, pad, row0;           // row0: first A row (s=1) / pair (s=2) loaded, multiple of 8
+  int ck, n_kchunks, rows;         // channels per k-chunk, A rows per (parity, group) region
   int mt_per_p, num_tiles;
   uint32_t a_stage_bytes, b_chunk_bytes;
   int na_stages, nb_slots, b_resident;
   uint32_t tmem_cols;
   const uint8_t* wpack;            // [ntile][kchunk][kstep][2][bn][16 B] fp16
   const float* bias;               // [n_ntiles*bn] (zero padded)
-  __half* out;                     // NG8 [P][cout/8][lp_out][8]
-  const __half* res;               // shortcut source (NG8) or null
-  int res_mode;                    // 0 none, 1 identity, 2 maxpool(2)
-  int res_c, lp_res;
+  __half* out;                     // output activation (layout out_split)
+  const __half* res;               // shortcut source or null
+  int res_mode;                    // 0 none, 1 identity (I layout), 2 maxpool(2) (S layout)
+  int res_c, res_rows;             // shortcut channels; plane rows (I: lp, S: lh)
   int relu;
   const float* fc_w;               // head: [cout] -> head_out[P][mt_per_p] (null = no head)
   float* head_out;
+  int dbg;                         // experiments only (HB_DEBUG env)
+  unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]
 };
 
 struct ConvPlan {
@@ -46,10 +62,12 @@ struct ConvPlan {
   uint32_t smem_bytes;
 };
 
-// Build a plan (tensor map + tiling) for one conv layer.  Returns 0 or an error string.
+// Build a plan (tensor map + tiling) for one conv layer.  The input layout is
+// I for stride 1 and S for stride 2; res (if any) is I for identity, S for
+// maxpool; `out_split` selects the output layout.  Returns 0 or an error string.
 const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lout, int stride, int pad,
-                      const __half* in, int lp_in, __half* out, const uint8_t* wpack, const float* bias,
-                      const __half* res, int res_mode, int res_c, int lp_res, const float* fc_w,
+                      const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
+                      const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
                       float* head_out, int num_sms);
 // Host-side packing of canonical weights W[cout][cin][16] into the plan's B image.
 size_t wpack_bytes(int cin, int cout);

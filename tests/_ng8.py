@@ -18,3 +18,26 @@ def to_ng8(x: torch.Tensor) -> torch.Tensor:
 def from_ng8(a: torch.Tensor, C: int, L: int) -> torch.Tensor:
     P = a.shape[0]
     return a[:, :, :L, :].permute(0, 1, 3, 2).reshape(P, C, L)
+
+
+def lh(length: int) -> int:
+    return ((length + 1) // 2 + 7) // 8 * 8
+
+
+def to_split(x: torch.Tensor) -> torch.Tensor:
+    """[P, C, L] -> parity-split S layout [P, C/8, 2, Lh, 8] fp16 (even / odd positions), zero padded."""
+    P, C, L = x.shape
+    h = lh(L)
+    out = torch.zeros(P, C // 8, 2, h, 8, dtype=torch.float16, device=x.device)
+    g = x.reshape(P, C // 8, 8, L).permute(0, 1, 3, 2).to(torch.float16)  # [P, G, L, 8]
+    out[:, :, 0, : (L + 1) // 2, :] = g[:, :, 0::2, :]
+    out[:, :, 1, : L // 2, :] = g[:, :, 1::2, :]
+    return out.contiguous()
+
+
+def from_split(a: torch.Tensor, C: int, L: int) -> torch.Tensor:
+    P = a.shape[0]
+    g = torch.empty(P, C // 8, L, 8, dtype=a.dtype, device=a.device)
+    g[:, :, 0::2, :] = a[:, :, 0, : (L + 1) // 2, :]
+    g[:, :, 1::2, :] = a[:, :, 1, : L // 2, :]
+    return g.permute(0, 1, 3, 2).reshape(P, C, L)

@@ -12,7 +12,7 @@ import pytest
 import torch
 import torch.nn.functional as F
 
-from _ng8 import from_ng8, lp, to_ng8
+from _ng8 import from_ng8, from_split, lh, lp, to_ng8, to_split
 
 pytestmark = pytest.mark.gpu
 
@@ -40,15 +40,22 @@ def ref_conv(x, w, b, stride, res=None, res_mode=0, relu=True):
     return torch.relu(y) if relu else y
 
 
-def run_conv(x, w, b, stride, res=None, res_mode=0, fc_w=None):
+def run_conv(x, w, b, stride, res=None, res_mode=0, fc_w=None, out_split=0):
+    """Device conv through the C-ABI; layouts: stride-2 input and maxpool shortcut
+    in the parity-split layout, everything else interleaved."""
     L = _lib()
     P, cin, lin = x.shape
     cout = w.shape[0]
     lout = -(-lin // stride)
     dev = torch.device("cuda")
-    xin = to_ng8(x.to(dev))
-    out = torch.zeros(P, cout // 8, lp(lout), 8, dtype=torch.float16, device=dev)
-    rin = to_ng8(res.to(dev)) if res is not None else None
+    xin = to_split(x.to(dev)) if stride == 2 else to_ng8(x.to(dev))
+    if out_split:
+        out = torch.full((P, cout // 8, 2, lh(lout), 8), 7.0, dtype=torch.float16, device=dev)
+    else:
+        out = torch.full((P, cout // 8, lp(lout), 8), 7.0, dtype=torch.float16, device=dev)
+    rin = None
+    if res is not None:
+        rin = to_split(res.to(dev)) if res_mode == 2 else to_ng8(res.to(dev))
     head = torch.zeros(P, (lout + 127) // 128, dtype=torch.float32, device=dev) if fc_w is not None else None
     wn = np.ascontiguousarray(w.numpy(), np.float32)
     bn = np.ascontiguousarray(b.numpy(), np.float32)
@@ -57,7 +64,8 @@ def run_conv(x, w, b, stride, res=None, res_mode=0, fc_w=None):
         C.c_void_p(xin.data_ptr()), P, cin, lin, stride, L.fptr(wn), L.fptr(bn), cout,
         C.c_void_p(rin.data_ptr()) if rin is not None else None, res_mode,
         res.shape[1] if res is not None else 0, res.shape[2] if res is not None else 0,
-        C.c_void_p(out.data_ptr()), L.fptr(fcn), C.c_void_p(head.data_ptr()) if head is not None else None,
+        C.c_void_p(out.data_ptr()), int(out_split), L.fptr(fcn),
+        C.c_void_p(head.data_ptr()) if head is not None else None,
         C.c_void_p(torch.cuda.current_stream().cuda_stream))
     L.check(rc)
     torch.cuda.synchronize()
@@ -84,8 +92,9 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("out_split", [0, 1])
 @pytest.mark.parametrize("cin,cout,lin,stride,res_mode,P", CASES)
-def test_conv_matches_fp32(cin, cout, lin, stride, res_mode, P):
+def test_conv_matches_fp32(cin, cout, lin, stride, res_mode, P, out_split):
     g = torch.Generator().manual_seed(cin * 7 + cout + lin + stride)
     x = torch.relu(_rand((P, cin, lin), g))
     w = _rand((cout, cin, 16), g, (2.0 / (cin * 16)) ** 0.5)
@@ -93,14 +102,18 @@ def test_conv_matches_fp32(cin, cout, lin, stride, res_mode, P):
     res = None
     if res_mode == 1:
         res = torch.relu(_rand((P, min(cin, cout), -(-lin // stride)), g))
-    out, _, lout = run_conv(x, w, b, stride, res, res_mode)
+    out, _, lout = run_conv(x, w, b, stride, res, res_mode, out_split=out_split)
     ref = ref_conv(x, w, b, stride, res, res_mode)
-    got = from_ng8(out, cout, lout).float().cpu()
+    got = (from_split(out, cout, lout) if out_split else from_ng8(out, cout, lout)).float().cpu()
     err = (got - ref).abs()
     tol = 2e-3 * ref.abs() + 2e-3
     assert bool((err <= tol).all()), f"max err {err.max().item():.3e} at {torch.nonzero(err > tol)[:4].tolist()}"
-    # padded rows [lout, lp) must be zero (the next layer's TMA reads them)
-    assert bool((out[:, :, lout:, :] == 0).all())
+    # padding positions >= lout must be written as zero (the next layer's TMA reads them)
+    if out_split:
+        assert bool((out[:, :, 0, (lout + 1) // 2:, :] == 0).all())
+        assert bool((out[:, :, 1, lout // 2:, :] == 0).all())
+    else:
+        assert bool((out[:, :, lout:, :] == 0).all())
 
 
 @pytest.mark.parametrize("lin,res_len", [(3750, 7500), (938, 1875)])
@@ -116,6 +129,23 @@ def test_conv_maxpool_shortcut(lin, res_len):
     ref = ref_conv(x, w, b, 1, blk, 2)
     got = from_ng8(out, c, lout).float().cpu()
     assert torch.allclose(got, ref, rtol=2e-3, atol=2e-3), (got - ref).abs().max()
+
+
+@pytest.mark.parametrize("L", [128, 1024, 937, 7500])
+def test_layout_padding_edges(L):
+    """Lengths at / just off tile and 8-row boundaries, both output layouts."""
+    g = torch.Generator().manual_seed(L)
+    P, c = 2, 16
+    x = torch.relu(_rand((P, c, L), g))
+    w = _rand((c, c, 16), g, (2.0 / (c * 16)) ** 0.5)
+    b = _rand((c,), g, 0.1)
+    for split in (0, 1):
+        out, _, lout = run_conv(x, w, b, 1, out_split=split)
+        got = (from_split(out, c, lout) if split else from_ng8(out, c, lout)).float().cpu()
+        assert torch.allclose(got, ref_conv(x, w, b, 1), rtol=2e-3, atol=2e-3)
+        x2 = torch.relu(_rand((P, c, L), g))
+        out2, _, l2 = run_conv(x2, w, b, 2)
+        assert torch.allclose(from_ng8(out2, c, l2).float().cpu(), ref_conv(x2, w, b, 2), rtol=2e-3, atol=2e-3)
 
 
 def test_conv_fused_head():
