@@ -17,12 +17,13 @@
 //   with plain bulk copies; it stays resident in smem across tiles when the
 //   whole layer's weights fit.
 //
-// Roles (256 threads, 1 CTA/SM, persistent over tiles):
+// Roles (384 threads, 1 CTA/SM, persistent over tiles):
 //   warp 0  : TMA producer (one lane)
 //   warp 1  : MMA issuer (warp-uniform loop, one elected lane issues),
-//             double-buffered TMEM accumulators
+//             double-buffered TMEM accumulators (tile i of the CTA -> buffer i%2)
 //   warp 2  : TMEM allocator
-//   warps 4-7: epilogue, thread r <-> TMEM lane r <-> output position l0+r
+//   warps 4-7 / 8-11: two epilogue warpgroups, warpgroup e drains buffer e
+//             (every other tile); thread r <-> TMEM lane r <-> position l0+r
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
@@ -57,8 +58,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* acc_full = b_empty + a.nb_slots;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [4] per-warp head partials
-  float* s_bias = s_head + 4;                                  // [bn]
+  float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [2][4] per-warp head partials
+  float* s_bias = s_head + 8;                                  // [bn]
   float* s_fc = s_bias + 256;                                  // [bn]
 
   const uint32_t warp = warp_id();
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], 128);  // one epilogue warpgroup per buffer
     }
     fence_barrier_init();
   }
@@ -271,15 +272,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int wq = static_cast<int>(warp) - 4;
+    const int eg = (static_cast<int>(warp) - 4) >> 2;  // epilogue warpgroup = accumulator buffer
+    const int wq = static_cast<int>(warp) & 3;          // TMEM lane quadrant of this warp
     const int r = wq * 32 + static_cast<int>(lane);
-    int acc = 0;
+    const int acc = eg;
     uint32_t accph = 0;
     const int out_groups = a.cout / 8;
     const int res_groups = a.res_mode ? a.res_c / 8 : 0;
-    const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0;
+    const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0 && eg == 0;
     unsigned long long e_wait = 0, e_work = 0, et0 = 0, e_start = eprof ? clock64() : 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
       const int nt = tile / tiles_per_nt;
       const int rem = tile % tiles_per_nt;
       const int p = rem / a.mt_per_p;
@@ -386,20 +388,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
       if (eprof) e_work += clock64() - et0;
-      if (++acc == 2) {
-        acc = 0;
-        accph ^= 1;
-      }
+      accph ^= 1;
       if (a.fc_w != nullptr) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) head += __shfl_xor_sync(0xffffffffu, head, off);
-        if (lane == 0) s_head[wq] = head;
-        named_bar_sync(1, 128);
+        float* sh = s_head + 4 * eg;
+        if (lane == 0) sh[wq] = head;
+        named_bar_sync(1 + eg, 128);
         if (wq == 0 && lane == 0) {
-          const float sum = ((s_head[0] + s_head[1]) + s_head[2]) + s_head[3];
+          const float sum = ((sh[0] + sh[1]) + sh[2]) + sh[3];
           a.head_out[static_cast<size_t>(p) * a.mt_per_p + mt] = sum;  // n_ntiles == 1 enforced for heads
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1 + eg, 128);
       }
     }
     if (eprof) {

@@ -5,6 +5,7 @@
 #include "hb_kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -65,6 +66,7 @@ struct Member {
 
 struct hb_ctx {
   int device = 0, P = 0, leads = 0, fs = 0, W = 0, hop = 0, R = 0, keep = 0, num_sms = 148;
+  int max_lanes = 4;  // concurrent member branches in the tick graph (HB_LANES overrides)
   cudaStream_t own = nullptr;
   float* ring = nullptr;
   float* staged = nullptr;   // [P][leads][hop]
@@ -75,8 +77,13 @@ struct hb_ctx {
   float* stats = nullptr;    // [P][leads][2]
   std::map<int, Member> members;
   std::vector<int> selected;
-  // per-selection resources
-  __half* act[3] = {nullptr, nullptr, nullptr};
+  // per-selection resources: `lanes` concurrent member branches, 3 rotating
+  // activation buffers each (members on one branch run back to back)
+  int lanes = 1;
+  std::vector<__half*> act;
+  std::vector<int> member_lane;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> ev;
   size_t act_bytes = 0;
   HeadMember* d_heads = nullptr;
   float* member_logits = nullptr;
@@ -106,10 +113,13 @@ cudaStream_t pick(hb_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) 
 void free_selection(hb_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   c->graph = nullptr;
-  for (auto& a : c->act) {
-    if (a) cudaFree(a);
-    a = nullptr;
-  }
+  for (auto& a : c->act) cudaFree(a);
+  c->act.clear();
+  for (auto s2 : c->side) cudaStreamDestroy(s2);
+  c->side.clear();
+  for (auto e : c->ev) cudaEventDestroy(e);
+  c->ev.clear();
+  c->member_lane.clear();
   c->act_bytes = 0;
   if (c->d_heads) cudaFree(c->d_heads);
   if (c->member_logits) cudaFree(c->member_logits);
@@ -156,19 +166,35 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   CK(c, launch_ingest_window(c->staged, c->ring, c->wpos, c->P, c->leads, c->hop, c->R, c->W, c->xn,
                              c->keep ? c->raw : nullptr, c->stats, st));
   pr->mark(st, K_INGEST, 0.0, P * c->leads * (c->hop * 8.0 + c->W * 6.0));
+  // Members fork into `lanes` branches after the window kernel and join before
+  // the aggregate (captured as parallel graph branches).  The eager profiling
+  // path (pr->ev set) keeps everything on one stream so per-kernel event times
+  // stay clean.
+  const bool fork = (pr->ev == nullptr) && c->lanes > 1;
+  if (fork) CK(c, cudaEventRecord(c->ev[0], st));
   size_t pi = 0;
-  for (int idx : c->selected) {
-    Member& m = c->members[idx];
+  for (size_t mi = 0; mi < c->selected.size(); ++mi) {
+    Member& m = c->members[c->selected[mi]];
+    const int ln = c->member_lane[mi];
+    cudaStream_t ms = fork ? c->side[ln] : st;
+    if (fork && mi < static_cast<size_t>(c->lanes)) CK(c, cudaStreamWaitEvent(ms, c->ev[0], 0));
+    __half* const* act = &c->act[3 * ln];
     const LayerSpec& s0 = m.layers[0];
     CK(c, launch_stem(c->xn + static_cast<size_t>(m.lead) * c->P * c->W, c->W, c->P, c->W,
-                      round_up(s0.lout, 8), s0.cout, s0.pad, m.stem_w, m.stem_b, c->act[0], st));
-    pr->mark(st, K_STEM, P * 2.0 * s0.cout * kTaps * s0.lout, P * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+                      round_up(s0.lout, 8), s0.cout, s0.pad, m.stem_w, m.stem_b, act[0], ms));
+    pr->mark(ms, K_STEM, P * 2.0 * s0.cout * kTaps * s0.lout, P * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
     for (size_t li = 1; li < m.layers.size(); ++li) {
       const LayerSpec& L = m.layers[li];
-      CK(c, launch_conv(c->plans[pi++], st));
-      pr->mark(st, K_CONV, P * 2.0 * L.cin * L.cout * kTaps * L.lout,
+      CK(c, launch_conv(c->plans[pi++], ms));
+      pr->mark(ms, K_CONV, P * 2.0 * L.cin * L.cout * kTaps * L.lout,
                P * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
                           (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
+    }
+  }
+  if (fork) {
+    for (int ln = 0; ln < c->lanes; ++ln) {
+      CK(c, cudaEventRecord(c->ev[1 + ln], c->side[ln]));
+      CK(c, cudaStreamWaitEvent(st, c->ev[1 + ln], 0));
     }
   }
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
@@ -184,22 +210,38 @@ int build_selection(hb_ctx* c) {
   free_selection(c);
   if (c->selected.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
   // activation buffers sized for the largest layer output of any selected member
+  const int M = static_cast<int>(c->selected.size());
+  c->lanes = std::max(1, std::min(M, c->max_lanes));
   size_t need = 0;
   for (int idx : c->selected)
     for (auto& L : c->members[idx].layers)
       need = std::max(need, static_cast<size_t>(c->P) * L.cout * act_rows(L.lout, 1) * sizeof(__half));
+  c->act.assign(3 * c->lanes, nullptr);
   for (auto& a : c->act) {
     CK(c, cudaMalloc(&a, need));
     CK(c, cudaMemset(a, 0, need));
   }
   c->act_bytes = need;
-  const int M = static_cast<int>(c->selected.size());
+  // greedy FLOP balance of members over lanes (zoo order kept within a lane)
+  {
+    std::vector<double> load(c->lanes, 0.0);
+    for (int idx : c->selected) {
+      const int ln = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+      c->member_lane.push_back(ln);
+      load[ln] += c->members[idx].flops;
+    }
+  }
+  c->side.resize(c->lanes);
+  for (auto& s2 : c->side) CK(c, cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  c->ev.resize(1 + c->lanes);
+  for (auto& e : c->ev) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(c, cudaMalloc(&c->member_logits, sizeof(float) * c->P * M));
   CK(c, cudaMalloc(&c->ens_prob, sizeof(float) * c->P));
   CK(c, cudaMalloc(&c->ens_logit, sizeof(float) * c->P));
   std::vector<HeadMember> heads;
-  for (int idx : c->selected) {
-    Member& m = c->members[idx];
+  for (size_t mi = 0; mi < c->selected.size(); ++mi) {
+    Member& m = c->members[c->selected[mi]];
+    __half* const* act = &c->act[3 * c->member_lane[mi]];
     int cur = 0;
     const int nblocks = static_cast<int>(m.layers.size() - 1) / 2;
     for (size_t li = 1; li < m.layers.size(); ++li) {
@@ -213,14 +255,14 @@ int build_selection(hb_ctx* c) {
       } else {
         src = (cur + 1) % 3;
         dst = (cur + 2) % 3;
-        res = c->act[cur];
+        res = act[cur];
         res_len = m.layers[li - 1].lin;
         // the output of an even block feeds the next (stride-2) block: parity-split layout
         out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
       }
       ConvPlan plan;
-      const char* e = plan_conv(&plan, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, c->act[src],
-                                L.head ? nullptr : c->act[dst], out_split, m.wpack[li - 1], m.bias[li - 1], res,
+      const char* e = plan_conv(&plan, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+                                L.head ? nullptr : act[dst], out_split, m.wpack[li - 1], m.bias[li - 1], res,
                                 conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? m.fc_w : nullptr,
                                 L.head ? m.head_partial : nullptr, c->num_sms);
       if (e) return fail(c, HB_E_INVALID, e);
@@ -279,6 +321,7 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   c->hop = cfg->hop;
   c->R = cfg->ring_len > 0 ? cfg->ring_len : round_up(cfg->window_len + cfg->hop, 256);
   c->keep = cfg->keep_windows;
+  if (getenv("HB_LANES")) c->max_lanes = std::max(1, atoi(getenv("HB_LANES")));
   if (c->R < c->W) {
     delete c;
     return fail(nullptr, HB_E_CONFIG, "ring_len must be >= window_len");

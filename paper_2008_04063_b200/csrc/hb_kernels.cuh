@@ -14,7 +14,7 @@ namespace hb {
 
 constexpr int kTaps = 16;
 constexpr int kBM = 128;               // output positions per tile (UMMA M)
-constexpr int kConvThreads = 256;      // warp0 TMA, warp1 MMA, warp2 TMEM, warps4-7 epilogue
+constexpr int kConvThreads = 384;      // warp0 TMA, warp1 MMA, warp2 TMEM, warps 4-7 / 8-11 epilogue
 constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic smem on sm_100
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
