@@ -1,5 +1,5 @@
 import sys, ctypes as C
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2008_04063_b200 import _lib
 L = _lib.lib()
 shapes = [(64, c, c, l, s, r) for (c, l, s, r) in [(32,7500,1,0),(32,7500,1,1),(64,7500,1,0),(64,7500,1,1),(64,3750,2,0),(128,3750,1,0),(256,1875,1,0)]]

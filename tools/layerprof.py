@@ -1,5 +1,5 @@
 import sys, numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2008_04063_b200.engine import EnsembleEngine
 from paper_2008_04063_b200.zoo import Selector, holmes_zoo
 from paper_2008_04063_b200 import arch
