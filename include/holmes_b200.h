@@ -101,6 +101,13 @@ int hb_stage_device(hb_ctx* ctx, const float* dev_samples, void* stream);
 int hb_tick_device(hb_ctx* ctx, void* stream);
 int hb_device_outputs(const hb_ctx* ctx, float** member_logits, float** ens_prob, float** ens_mean_logit);
 
+/* Device milliseconds of the most recent tick graph (CUDA events on the tick's
+ * stream around the graph launch; waits for the tick to finish). */
+int hb_last_tick_ms(hb_ctx* ctx, float* ms);
+/* Median device milliseconds of `reps` tick-graph launches on the context's
+ * stream (after one warm-up launch).  Measures; the stream cursor advances. */
+int hb_time_tick(hb_ctx* ctx, int reps, float* median_ms);
+
 /* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
  * (mean, std) [P][n_leads][2] of the most recent tick. */
 int hb_last_windows(hb_ctx* ctx, float* raw, float* stats, void* stream);
@@ -113,10 +120,32 @@ int hb_profile_tick(hb_ctx* ctx, void* stream, int cap, int* kinds, float* ms, d
 /* Algorithmic work of one tick: conv FLOPs and activation bytes (all selected members). */
 int hb_tick_work(const hb_ctx* ctx, double* flops, double* bytes);
 
-/* Profiler sweep: exact ROC-AUC (Mann-Whitney U from midranks, ties half
- * credit) of the ensemble mean scores[:, sel].mean(1) for every selector.
- * scores [N][n] fp64 row-major, labels[N] in {0,1}, selectors[S] bitmasks
- * (bit k <-> column k, n <= 32).  Host buffers in and out. */
+/* ---------------------------------------------------------------- K6 sweep
+ * Profiler sweep over a recorded cohort (replaces exhaustive_search's batched
+ * accuracy pass `roc_auc_many(labels, scores @ bits.T / pop)`,
+ * pkg/src/zooserve/composer.py:614-619, and the accuracy profiler
+ * `ensemble_roc_auc`, cohort.py:100-102 / composer.py:301-302).
+ * A cohort is scores[N][n] fp64 row-major (caller-owned, copied to the
+ * device once) + labels[N] in {0,1}.  AUC = exact Mann-Whitney U from
+ * midranks (ties half credit, metrics.py:30-60) of the ensemble mean
+ * scores[:, sel].mean(1), summed in fp64 in column order.
+ * Errors: labels not 0/1 or non-finite scores -> HB_E_INVALID (ValueError);
+ * one class only -> HB_E_METRIC (UndefinedMetricError); an all-zero selector
+ * -> HB_E_EMPTY (EmptyEnsembleError). */
+typedef struct hb_cohort hb_cohort;
+int hb_cohort_create(int device, const double* scores, const int8_t* labels, int N, int n, hb_cohort** out);
+int hb_cohort_destroy(hb_cohort* c);
+/* Last error of c, or of the calling thread's last failed cohort call when c is NULL. */
+const char* hb_cohort_last_error(const hb_cohort* c);
+/* Explicit selectors: bits[S][n] (0/1, bit k <-> column k) -> auc_out[S]. */
+int hb_cohort_auc(hb_cohort* c, const uint8_t* bits, int S, double* auc_out);
+/* Enumerated selectors: values first .. first+count-1 (bit k of the value <->
+ * column k, LSB = column 0; n <= 63) -> auc_out[count].  exhaustive_search
+ * is (first=1, count=2^n-1), composer.py:615-616. */
+int hb_cohort_auc_range(hb_cohort* c, unsigned long long first, long long count, double* auc_out);
+/* One selector: the ensemble means ens_out[N] (original row order) and its AUC. */
+int hb_cohort_ensemble(hb_cohort* c, const uint8_t* bits, double* ens_out, double* auc_out);
+/* One-shot convenience: selectors[S] as 32-bit masks (n <= 32). */
 int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
                  int S, double* auc_out);
 

@@ -49,12 +49,21 @@ _SIGS = {
     "hb_stage_device": (C.c_int, [_P, _P, _P]),
     "hb_tick_device": (C.c_int, [_P, _P]),
     "hb_device_outputs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "hb_last_tick_ms": (C.c_int, [_P, _F]),
+    "hb_time_tick": (C.c_int, [_P, C.c_int, _F]),
     "hb_last_windows": (C.c_int, [_P, _F, _F, _P]),
     "hb_profile_tick": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int), _F, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]),
     "hb_tick_work": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hb_sweep_auc": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,
                                C.POINTER(C.c_uint32), C.c_int, C.POINTER(C.c_double)]),
+    "hb_cohort_create": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,
+                                   C.POINTER(_P)]),
+    "hb_cohort_destroy": (C.c_int, [_P]),
+    "hb_cohort_last_error": (C.c_char_p, [_P]),
+    "hb_cohort_auc": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_double)]),
+    "hb_cohort_auc_range": (C.c_int, [_P, C.c_ulonglong, C.c_longlong, C.POINTER(C.c_double)]),
+    "hb_cohort_ensemble": (C.c_int, [_P, C.POINTER(C.c_uint8), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hb_op_conv1d": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
                                C.c_int, _P, C.c_int, _F, _P, _P]),
     "hb_bench_conv": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
@@ -87,12 +96,18 @@ def exported_symbols() -> list[str]:
     return sorted(_SIGS)
 
 
-def check(rc: int, ctx=None) -> None:
+def check(rc: int, ctx=None, getter: str = "hb_last_error") -> None:
+    """Raise the reference's exception class for a non-zero status (errors.py)."""
     if rc == HB_OK:
         return
-    msg = lib().hb_last_error(ctx)
+    msg = getattr(lib(), getter)(ctx)
     text = msg.decode() if msg else f"status {rc}"
     raise _EXC.get(rc, RuntimeError)(text)
+
+
+def dptr(a):
+    """float64 numpy array -> POINTER(c_double)."""
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
 
 
 def fptr(a):

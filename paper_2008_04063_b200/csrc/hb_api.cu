@@ -91,6 +91,8 @@ struct hb_ctx {
   float* ens_logit = nullptr;
   std::vector<ConvPlan> plans;
   cudaGraphExec_t graph = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
+  bool timed = false;
   bool dirty = true;
   std::string err;
 };
@@ -336,7 +338,8 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
             cudaMalloc(&c->wpos, sizeof(long long)) == cudaSuccess &&
             cudaMemset(c->wpos, 0, sizeof(long long)) == cudaSuccess &&
             cudaMalloc(&c->xn, S * c->W * sizeof(__half)) == cudaSuccess &&
-            cudaMalloc(&c->stats, S * 2 * sizeof(float)) == cudaSuccess;
+            cudaMalloc(&c->stats, S * 2 * sizeof(float)) == cudaSuccess &&
+            cudaEventCreate(&c->t0) == cudaSuccess && cudaEventCreate(&c->t1) == cudaSuccess;
   if (ok && c->keep) ok = cudaMalloc(&c->raw, S * c->W * sizeof(float)) == cudaSuccess;
   if (!ok) {
     hb_destroy(c);
@@ -359,6 +362,8 @@ int hb_destroy(hb_ctx* c) {
   cudaFree(c->xn);
   cudaFree(c->raw);
   cudaFree(c->stats);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return HB_OK;
@@ -488,7 +493,11 @@ int hb_tick_device(hb_ctx* c, void* stream) {
   cudaSetDevice(c->device);
   const int rc = build_selection(c);
   if (rc) return rc;
-  CK(c, cudaGraphLaunch(c->graph, pick(c, stream)));
+  cudaStream_t st = pick(c, stream);
+  CK(c, cudaEventRecord(c->t0, st));
+  CK(c, cudaGraphLaunch(c->graph, st));
+  CK(c, cudaEventRecord(c->t1, st));
+  c->timed = true;
   return HB_OK;
 }
 
@@ -501,7 +510,10 @@ int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_pr
   if (rc) return rc;
   if (samples)
     CK(c, cudaMemcpyAsync(c->staged, samples, sizeof(float) * c->P * c->leads * c->hop, cudaMemcpyHostToDevice, st));
+  CK(c, cudaEventRecord(c->t0, st));
   CK(c, cudaGraphLaunch(c->graph, st));
+  CK(c, cudaEventRecord(c->t1, st));
+  c->timed = true;
   const size_t M = c->selected.size();
   bool any = false;
   if (member_logits) {
@@ -551,6 +563,37 @@ int hb_profile_tick(hb_ctx* c, void* stream, int cap, int* kinds, float* ms, dou
   cudaEventDestroy(start);
   if (rc) return rc;
   return n;
+}
+
+int hb_last_tick_ms(hb_ctx* c, float* ms) {
+  if (!c || !ms) return fail(c, HB_E_INVALID, "null argument");
+  if (!c->timed) return fail(c, HB_E_STATE, "no tick has run yet");
+  cudaSetDevice(c->device);
+  CK(c, cudaEventSynchronize(c->t1));
+  CK(c, cudaEventElapsedTime(ms, c->t0, c->t1));
+  return HB_OK;
+}
+
+int hb_time_tick(hb_ctx* c, int reps, float* median_ms) {
+  if (!c || !median_ms || reps < 1) return fail(c, HB_E_INVALID, "bad argument");
+  cudaSetDevice(c->device);
+  const int rc = build_selection(c);
+  if (rc) return rc;
+  cudaStream_t st = c->own;
+  // warm-up launch, then `reps` individually bracketed launches; the stream
+  // cursor advances like a real tick (the data is whatever the rings hold)
+  CK(c, cudaGraphLaunch(c->graph, st));
+  std::vector<float> t(reps);
+  for (int i = 0; i < reps; ++i) {
+    CK(c, cudaEventRecord(c->t0, st));
+    CK(c, cudaGraphLaunch(c->graph, st));
+    CK(c, cudaEventRecord(c->t1, st));
+    CK(c, cudaEventSynchronize(c->t1));
+    CK(c, cudaEventElapsedTime(&t[i], c->t0, c->t1));
+  }
+  std::sort(t.begin(), t.end());
+  *median_ms = t[reps / 2];
+  return HB_OK;
 }
 
 int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {
@@ -741,12 +784,6 @@ int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b
   cudaFree(db);
   if (ce != cudaSuccess) return fail(none, HB_E_CUDA, cudaGetErrorString(ce));
   return HB_OK;
-}
-
-int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
-                 int S, double* auc_out) {
-  (void)device; (void)scores; (void)labels; (void)N; (void)n; (void)selectors; (void)S; (void)auc_out;
-  return fail(nullptr, HB_E_STATE, "hb_sweep_auc: not built yet");
 }
 
 }  // extern "C"

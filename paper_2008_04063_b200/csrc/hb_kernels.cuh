@@ -106,10 +106,4 @@ cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float*
                              float* ens_prob, float* ens_logit, cudaStream_t st);
 constexpr int kMaxMembers = 64;
 
-// profiler sweep (K6): exact midrank AUC of every selector's ensemble mean.
-cudaError_t launch_sweep_auc(const double* scores /*[N][n] row-major*/, const int8_t* labels, int N, int n,
-                             const uint32_t* selectors /*[S] bitmasks*/, int S, double* auc_out,
-                             void* scratch, size_t scratch_bytes, cudaStream_t st);
-size_t sweep_scratch_bytes(int N, int S);
-
 }  // namespace hb

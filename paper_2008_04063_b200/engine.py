@@ -168,6 +168,19 @@ class EnsembleEngine:
         n = min(n, cap)
         return kinds[:n], ms[:n], fl[:n], by[:n]
 
+    def last_tick_seconds(self) -> float:
+        """Device seconds of the most recent tick graph (CUDA events on its stream)."""
+        ms = C.c_float()
+        _lib.check(_lib.lib().hb_last_tick_ms(self._h, C.byref(ms)), self._h)
+        return ms.value / 1e3
+
+    def time_tick(self, reps: int = 5) -> float:
+        """Median device seconds of `reps` tick launches (measurement only; advances the stream)."""
+        ms = C.c_float()
+        with self._lock:
+            _lib.check(_lib.lib().hb_time_tick(self._h, int(reps), C.byref(ms)), self._h)
+        return ms.value / 1e3
+
     def tick_work(self) -> tuple[float, float]:
         """(conv FLOPs, activation bytes) of one tick for the current selector."""
         f, b = C.c_double(), C.c_double()

@@ -1,0 +1,91 @@
+"""Classification metrics of the drop-in surface.
+
+`roc_auc` / `roc_auc_many` keep the reference's signatures, validation and
+exceptions (`pkg/src/zooserve/metrics.py:16-76`) but are computed by the K6
+sweep kernel (`csrc/sweep.cu`): exact Mann-Whitney U from midranks with half
+credit for ties, so values are bit-identical to the reference's.  There is no
+CPU fallback for them.
+
+`pr_auc` and `f1_accuracy` (`metrics.py:79-111`) only feed the one-off
+accuracy report (`cohort.accuracy_profile`), never a per-tick or
+per-candidate path, so they stay plain numpy on the host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import UndefinedMetricError
+
+
+def validate(labels, scores) -> tuple[np.ndarray, np.ndarray]:
+    """1-D, same length, non-empty, labels in {0,1}, finite scores (metrics.py:16-27)."""
+    lab = np.asarray(labels)
+    sc = np.asarray(scores, dtype=np.float64)
+    if lab.ndim != 1 or lab.shape != sc.shape:
+        raise ValueError("labels and scores must be 1-D and the same length")
+    if lab.size == 0:
+        raise ValueError("need at least one sample")
+    if not np.isin(lab, (0, 1)).all():
+        raise ValueError("labels must be 0 or 1")
+    if not np.isfinite(sc).all():
+        raise ValueError("scores must be finite")
+    return lab.astype(np.int8), sc
+
+
+def _both_classes(lab: np.ndarray) -> None:
+    pos = int(lab.sum())
+    if pos == 0 or pos == lab.size:
+        raise UndefinedMetricError("roc_auc needs both classes present")
+
+
+def roc_auc(labels, scores, device: int = 0) -> float:
+    """P(score_pos > score_neg) + 0.5 P(tie), on the device."""
+    from .cohort import DeviceCohort
+    lab, sc = validate(labels, scores)
+    _both_classes(lab)
+    with DeviceCohort(sc[:, None], lab, device=device) as dc:
+        return float(dc.auc_bits(np.ones((1, 1), np.uint8))[0])
+
+
+def roc_auc_many(labels, score_matrix, device: int = 0) -> np.ndarray:
+    """roc_auc of every column against shared labels (metrics.py:63-76), one device pass."""
+    from .cohort import DeviceCohort
+    lab = np.asarray(labels).astype(np.int8)
+    mat = np.asarray(score_matrix, dtype=np.float64)
+    if mat.ndim != 2 or mat.shape[0] != lab.size:
+        raise ValueError("score_matrix must be (n_samples, n_columns)")
+    _both_classes(lab)
+    out = np.empty(mat.shape[1])
+    step = 256
+    for c0 in range(0, mat.shape[1], step):
+        block = np.ascontiguousarray(mat[:, c0:c0 + step])
+        k = block.shape[1]
+        with DeviceCohort(block, lab, device=device) as dc:
+            out[c0:c0 + k] = dc.auc_bits(np.eye(k, dtype=np.uint8))
+    return out
+
+
+def pr_auc(labels, scores) -> float:
+    """Average precision: step curve over descending score, tied scores enter together."""
+    lab, sc = validate(labels, scores)
+    n_pos = int(lab.sum())
+    if n_pos == 0:
+        raise UndefinedMetricError("pr_auc needs at least one positive")
+    order = np.argsort(-sc, kind="stable")
+    y, s = lab[order].astype(np.float64), sc[order]
+    tp, fp = np.cumsum(y), np.cumsum(1.0 - y)
+    keep = np.r_[s[1:] != s[:-1], True]     # last sample of every distinct score
+    tp, fp = tp[keep], fp[keep]
+    recall = tp / n_pos
+    return float(np.dot(np.diff(recall, prepend=0.0), tp / (tp + fp)))
+
+
+def f1_accuracy(labels, scores, threshold: float = 0.5) -> tuple[float, float]:
+    """(F1, accuracy) of the predictions score > threshold; F1 is 0 when undefined."""
+    lab, sc = validate(labels, scores)
+    pred, actual = sc > threshold, lab == 1
+    tp = int(np.sum(pred & actual))
+    wrong = int(np.sum(pred != actual))
+    denom = 2 * tp + wrong
+    return ((2 * tp / denom) if denom else 0.0), float(np.mean(pred == actual))
