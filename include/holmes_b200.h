@@ -100,6 +100,14 @@ int hb_tick(hb_ctx* ctx, const float* samples, float* member_logits, float* ens_
 int hb_stage_device(hb_ctx* ctx, const float* dev_samples, void* stream);
 int hb_tick_device(hb_ctx* ctx, void* stream);
 int hb_device_outputs(const hb_ctx* ctx, float** member_logits, float** ens_prob, float** ens_mean_logit);
+/* Member-sharded serving (several contexts / GPUs each running a subset of
+ * the ensemble): every tick also writes per-patient partial sums
+ * sums[2][P] = (sum of member sigmoids, sum of member logits) over this
+ * context's members, fixed order.  After a cross-rank SUM reduce,
+ * hb_finalize_sums turns them into the ensemble outputs over the total
+ * popcount (device pointers, stream-ordered). */
+int hb_device_sums(const hb_ctx* ctx, float** sums);
+int hb_finalize_sums(const float* sums, int P, int m_total, float* prob, float* logit, void* stream);
 
 /* Device milliseconds of the most recent tick graph (CUDA events on the tick's
  * stream around the graph launch; waits for the tick to finish). */

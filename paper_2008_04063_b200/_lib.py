@@ -51,6 +51,8 @@ _SIGS = {
     "hb_device_outputs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
     "hb_last_tick_ms": (C.c_int, [_P, _F]),
     "hb_time_tick": (C.c_int, [_P, C.c_int, _F]),
+    "hb_device_sums": (C.c_int, [_P, C.POINTER(_P)]),
+    "hb_finalize_sums": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     "hb_last_windows": (C.c_int, [_P, _F, _F, _P]),
     "hb_profile_tick": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int), _F, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]),

@@ -89,6 +89,7 @@ struct hb_ctx {
   float* member_logits = nullptr;
   float* ens_prob = nullptr;
   float* ens_logit = nullptr;
+  float* ens_sums = nullptr;  // [2][P]: sum of member sigmoids, sum of member logits
   std::vector<ConvPlan> plans;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
@@ -127,8 +128,9 @@ void free_selection(hb_ctx* c) {
   if (c->member_logits) cudaFree(c->member_logits);
   if (c->ens_prob) cudaFree(c->ens_prob);
   if (c->ens_logit) cudaFree(c->ens_logit);
+  if (c->ens_sums) cudaFree(c->ens_sums);
   c->d_heads = nullptr;
-  c->member_logits = c->ens_prob = c->ens_logit = nullptr;
+  c->member_logits = c->ens_prob = c->ens_logit = c->ens_sums = nullptr;
   c->plans.clear();
 }
 
@@ -200,7 +202,7 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
     }
   }
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
-                         c->ens_logit, st));
+                         c->ens_logit, c->ens_sums, st));
   pr->mark(st, K_AGG, 0.0, 0.0);
   CK(c, launch_advance(c->wpos, c->hop, st));
   pr->mark(st, K_ADV, 0.0, 0.0);
@@ -240,6 +242,7 @@ int build_selection(hb_ctx* c) {
   CK(c, cudaMalloc(&c->member_logits, sizeof(float) * c->P * M));
   CK(c, cudaMalloc(&c->ens_prob, sizeof(float) * c->P));
   CK(c, cudaMalloc(&c->ens_logit, sizeof(float) * c->P));
+  CK(c, cudaMalloc(&c->ens_sums, sizeof(float) * 2 * c->P));
   std::vector<HeadMember> heads;
   for (size_t mi = 0; mi < c->selected.size(); ++mi) {
     Member& m = c->members[c->selected[mi]];
@@ -601,6 +604,19 @@ int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {
   if (ml) *ml = c->member_logits;
   if (ep) *ep = c->ens_prob;
   if (el) *el = c->ens_logit;
+  return HB_OK;
+}
+
+int hb_device_sums(const hb_ctx* c, float** sums) {
+  if (!c || !c->ens_sums || !sums) return HB_E_STATE;
+  *sums = c->ens_sums;
+  return HB_OK;
+}
+
+int hb_finalize_sums(const float* sums, int P, int m_total, float* prob, float* logit, void* stream) {
+  if (!sums || !prob || !logit || P < 1 || m_total < 1) return fail(nullptr, HB_E_INVALID, "bad argument");
+  const cudaError_t e = launch_finalize(sums, P, m_total, prob, logit, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(nullptr, HB_E_CUDA, cudaGetErrorString(e));
   return HB_OK;
 }
 

@@ -160,7 +160,8 @@ cudaError_t launch_stem(const __half* xn, int x_stride, int P, int L, int lp_out
 __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __restrict__ mem, int M, int P,
                                                         float* __restrict__ member_logits,
                                                         float* __restrict__ ens_prob,
-                                                        float* __restrict__ ens_logit) {
+                                                        float* __restrict__ ens_logit,
+                                                        float* __restrict__ ens_sums) {
   __shared__ float s_logit[kMaxMembers];
   const int p = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,13 +184,29 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __rest
     }
     ens_prob[p] = sp / static_cast<float>(M);
     ens_logit[p] = sl / static_cast<float>(M);
+    ens_sums[p] = sp;       // member-sharded serving reduces these across ranks
+    ens_sums[P + p] = sl;
   }
 }
 
 cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits, float* ens_prob,
-                             float* ens_logit, cudaStream_t st) {
+                             float* ens_logit, float* ens_sums, cudaStream_t st) {
   if (M < 1 || M > kMaxMembers) return cudaErrorInvalidValue;
-  aggregate_kernel<<<P, 256, 0, st>>>(members_dev, M, P, member_logits, ens_prob, ens_logit);
+  aggregate_kernel<<<P, 256, 0, st>>>(members_dev, M, P, member_logits, ens_prob, ens_logit, ens_sums);
+  return cudaGetLastError();
+}
+
+// Member-sharded finish: sums[2][P] reduced over ranks -> means over the total popcount.
+__global__ void finalize_kernel(const float* __restrict__ sums, int P, float inv_m, float* __restrict__ prob,
+                                float* __restrict__ logit) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  prob[p] = sums[p] * inv_m;
+  logit[p] = sums[P + p] * inv_m;
+}
+
+cudaError_t launch_finalize(const float* sums, int P, int m_total, float* prob, float* logit, cudaStream_t st) {
+  finalize_kernel<<<(P + 255) / 256, 256, 0, st>>>(sums, P, 1.f / static_cast<float>(m_total), prob, logit);
   return cudaGetLastError();
 }
 

@@ -84,3 +84,24 @@ def test_measured_latency_profiler():
     assert 0 < t1 < t2 < 0.2
     rep = mp.report(Selector.from_indices(60, [10, 13]))
     assert rep.feasible and rep.total_s < 0.2
+
+
+def test_serving_loop_realtime():
+    """Wall-clock mode (runtime.py:321-396 counterpart): frames at 100x real time, one tick per hop."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    from paper_2008_04063_b200.serving import ServingLoop, frames_from, tick_latency_percentiles
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [10, 13])
+    P, hop, n_ticks = 8, 250, 12
+    streams = synth.ecg_block(6, P, 3, 0, 7500 + hop * n_ticks)
+    with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+        loop = ServingLoop(eng, frames_from(streams), speedup=100.0)
+        tr = loop.run(n_ticks)
+    assert len(tr) == P * n_ticks
+    assert [t.query_id for t in tr] == list(range(P * n_ticks))
+    pc = tick_latency_percentiles(tr, P)
+    assert pc["p99"] < 0.2
+    ml, _, _ = cpu_path.cpu_tick(zoo, sel, streams, 7500 + hop * n_ticks)
+    last = tr[-P:]
+    got = np.array([[t.model_scores[zoo.profiles[i].id] for i in sel.indices()] for t in last])
+    assert np.abs(got - ml).max() <= 2e-2
