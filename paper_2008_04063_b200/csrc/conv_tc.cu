@@ -45,6 +45,24 @@ __device__ __forceinline__ size_t out_offset(const ConvArgs& a, int p, int g, in
   return ((plane * 2 + (l & 1)) * a.out_lh + (l >> 1)) * 8;
 }
 
+// Tile order: member g of the group (slowest), N tile, patient, M tile.
+struct TileIdx {
+  int g, nt, p, mt;  // p = global row of the [G*Pm] activation tensors
+};
+__device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile) {
+  const int per_nt = a.Pm * a.mt_per_p;
+  const int per_g = a.n_ntiles * per_nt;
+  TileIdx t;
+  t.g = tile / per_g;
+  int rem = tile - t.g * per_g;
+  t.nt = rem / per_nt;
+  rem -= t.nt * per_nt;
+  const int pl = rem / a.mt_per_p;
+  t.mt = rem - pl * a.mt_per_p;
+  t.p = t.g * a.Pm + pl;
+  return t;
+}
+
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ ConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -82,16 +100,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
+  const bool uniform_bias = (a.n_ntiles == 1 && a.G == 1);  // bias / fc cached in smem
   for (int i = threadIdx.x; i < a.bn; i += blockDim.x) {
-    s_bias[i] = a.bias[i];
-    s_fc[i] = a.fc_w ? a.fc_w[i < a.cout ? i : 0] : 0.f;
+    s_bias[i] = uniform_bias ? a.bias[i] : 0.f;
+    s_fc[i] = (a.fc_w && uniform_bias) ? a.fc_w[i < a.cout ? i : 0] : 0.f;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Programmatic dependent launch: let the next layer's CTAs start their
+  // prologue as SMs free up; everything that reads the previous layer's
+  // output or writes ours happens after griddepcontrol.wait.
+  pdl_trigger();
 
-  const int tiles_per_nt = a.P * a.mt_per_p;
   const int groups = a.ck / 8;
   const uint32_t region_bytes = static_cast<uint32_t>(groups * a.rows * 16);
 
@@ -102,21 +124,39 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       uint32_t aph = 0;
       int bs = 0;
       uint32_t bph = 0;
-      int loaded_nt = -1;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-        const int nt = tile / tiles_per_nt;
-        const int rem = tile % tiles_per_nt;
-        const int p = rem / a.mt_per_p;
-        const int blk = ((rem % a.mt_per_p) * kBM + a.row0) / 8;  // first 128-B line (8 rows)
-        const bool load_b = !a.b_resident || nt != loaded_nt;
-        loaded_nt = nt;
+      int loaded_key = -1;
+      auto b_src = [&](const TileIdx& t, int kc) {
+        return a.wpack + static_cast<size_t>(t.g) * a.wpack_stride +
+               (static_cast<size_t>(t.nt) * a.n_kchunks + kc) * a.b_chunk_bytes;
+      };
+      // Weights are immutable: the first tile's resident B goes out before the
+      // dependency wait, overlapping the previous layer's tail.
+      if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {
+        const TileIdx t0 = decode_tile(a, blockIdx.x);
+        for (int kc = 0; kc < a.n_kchunks; ++kc) {
+          mbar_arrive_expect_tx(&b_full[kc], a.b_chunk_bytes);
+          bulk_load(sB + static_cast<size_t>(kc) * a.b_chunk_bytes, b_src(t0, kc), a.b_chunk_bytes, &b_full[kc]);
+        }
+        loaded_key = t0.g * a.n_ntiles + t0.nt;
+      }
+      pdl_wait();
+      int li = 0;  // local tile count
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++li) {
+        const TileIdx t = decode_tile(a, tile);
+        const int p = t.p;
+        const int blk = (t.mt * kBM + a.row0) / 8;  // first 128-B line (8 rows)
+        const int key = t.g * a.n_ntiles + t.nt;
+        const bool load_b = !a.b_resident || key != loaded_key;
+        // Reloading resident weights (next member of the group): the previous
+        // tile's MMAs must have drained out of the B slots first.
+        if (a.b_resident && load_b && li > 0) mbar_wait(&acc_full[(li - 1) & 1], ((li - 1) >> 1) & 1);
+        loaded_key = key;
         for (int kc = 0; kc < a.n_kchunks; ++kc) {
           if (load_b) {
             const int slot = a.b_resident ? kc : bs;
             if (!a.b_resident) mbar_wait(&b_empty[bs], bph ^ 1);
             mbar_arrive_expect_tx(&b_full[slot], a.b_chunk_bytes);
-            bulk_load(sB + static_cast<size_t>(slot) * a.b_chunk_bytes,
-                      a.wpack + (static_cast<size_t>(nt) * a.n_kchunks + kc) * a.b_chunk_bytes, a.b_chunk_bytes,
+            bulk_load(sB + static_cast<size_t>(slot) * a.b_chunk_bytes, b_src(t, kc), a.b_chunk_bytes,
                       &b_full[slot]);
             if (!a.b_resident && ++bs == a.nb_slots) {
               bs = 0;
@@ -161,9 +201,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint32_t bph = 0;
     int acc = 0;
     uint32_t accph = 0;
+    uint32_t bres_ph = 0;  // phase of the resident B slots (flips on every reload)
+    int mkey = -1;
     unsigned long long t_acc = 0, t_a = 0, t_issue = 0, t0 = 0;
     const bool prof = (a.dbg & 8) && a.prof;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      if (a.b_resident) {
+        const TileIdx tt = decode_tile(a, tile);
+        const int key = tt.g * a.n_ntiles + tt.nt;
+        if (mkey >= 0 && key != mkey) bres_ph ^= 1;
+        mkey = key;
+      }
       if (prof) t0 = clock64();
       mbar_wait(&acc_empty[acc], accph ^ 1);
       if (prof) t_acc += clock64() - t0;
@@ -172,7 +220,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int kc = 0; kc < a.n_kchunks; ++kc) {
         const int slot = a.b_resident ? kc : bs;
         if (prof) t0 = clock64();
-        mbar_wait(&b_full[slot], a.b_resident ? 0u : bph);
+        mbar_wait(&b_full[slot], a.b_resident ? bres_ph : bph);
         mbar_wait(&a_full[as], aph);
         if (prof) {
           const unsigned long long t1 = clock64();
@@ -281,11 +329,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int res_groups = a.res_mode ? a.res_c / 8 : 0;
     const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0 && eg == 0;
     unsigned long long e_wait = 0, e_work = 0, et0 = 0, e_start = eprof ? clock64() : 0;
+    pdl_wait();
     for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
-      const int nt = tile / tiles_per_nt;
-      const int rem = tile % tiles_per_nt;
-      const int p = rem / a.mt_per_p;
-      const int mt = rem % a.mt_per_p;
+      const TileIdx ti = decode_tile(a, tile);
+      const int nt = ti.nt;
+      const int p = ti.p;
+      const int mt = ti.mt;
       const int l = mt * kBM + r;
       const bool valid = l < a.lout;
       const bool in_buf = l < a.out_rows;
@@ -315,7 +364,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
       }
-      const float* bias_t = (a.n_ntiles == 1) ? s_bias : a.bias + static_cast<size_t>(nt) * a.bn;
+      const float* bias_t =
+          uniform_bias ? s_bias : a.bias + static_cast<size_t>(ti.g) * a.bias_stride + static_cast<size_t>(nt) * a.bn;
+      const float* fc_t = uniform_bias ? s_fc : a.fc_w + static_cast<size_t>(ti.g) * a.cout;
       if (eprof) et0 = clock64();
       mbar_wait(&acc_full[acc], accph);
       if (eprof) {
@@ -373,7 +424,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           if (a.fc_w != nullptr) {
             if (valid) {
 #pragma unroll
-              for (int k = 0; k < 8; ++k) head = fmaf(y[k], s_fc[8 * j + k], head);
+              for (int k = 0; k < 8; ++k) head = fmaf(y[k], fc_t[8 * j + k], head);
             }
           } else if (in_buf) {
             uint4 pk;
@@ -521,16 +572,30 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lout, int stride, int pad,
+size_t bias_len(int cout) {
+  const int bn = conv_bn(cout);
+  return static_cast<size_t>(((round_up(cout, 16) + bn - 1) / bn) * bn);
+}
+
+bool pdl_enabled() {
+  static const bool on = !(getenv("HB_NO_PDL") && atoi(getenv("HB_NO_PDL")));
+  return on;
+}
+
+const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                       const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
                       const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
                       float* head_out, int num_sms) {
   std::memset(plan, 0, sizeof(*plan));
+  if (G < 1 || G > kMaxGroup || Pm < 1) return "conv: bad group shape";
+  const int P = G * Pm;
   if (cin % 8 || cout % 8) return "conv: channels must be multiples of 8";
   if (stride != 1 && stride != 2) return "conv: stride must be 1 or 2";
   if (lout != (lin + stride - 1) / stride) return "conv: lout must be ceil(lin/stride)";
   ConvArgs& a = plan->args;
   a.P = P;
+  a.G = G;
+  a.Pm = Pm;
   a.cin = cin;
   a.cout = cout;
   a.bn = conv_bn(cout);
@@ -575,7 +640,9 @@ const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lou
   while (cols < static_cast<uint32_t>(2 * a.bn)) cols <<= 1;
   a.tmem_cols = cols;
   a.wpack = wpack;
+  a.wpack_stride = wpack_bytes(cin, cout);
   a.bias = bias;
+  a.bias_stride = static_cast<int>(bias_len(cout));
   a.out = out;
   a.res = res;
   a.res_mode = res ? res_mode : 0;
@@ -591,21 +658,21 @@ const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lou
 
   EncodeTiledFn enc = get_encode();
   if (!enc) return "conv: cuTensorMapEncodeTiled unavailable";
-  const cuuint64_t G = static_cast<cuuint64_t>(cin / 8);
+  const cuuint64_t CG = static_cast<cuuint64_t>(cin / 8);
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult rc;
   if (stride == 1) {  // I layout: [P][G][lp][8] as {64 elems = 8 rows, lp/8 lines, G, P}
     const cuuint64_t lp = static_cast<cuuint64_t>(lp_I(lin));
-    const cuuint64_t dims[4] = {64, lp / 8, G, static_cast<cuuint64_t>(P)};
-    const cuuint64_t strides[3] = {128, lp * 16, G * lp * 16};
+    const cuuint64_t dims[4] = {64, lp / 8, CG, static_cast<cuuint64_t>(P)};
+    const cuuint64_t strides[3] = {128, lp * 16, CG * lp * 16};
     const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(a.rows / 8), static_cast<cuuint32_t>(a.ck / 8), 1};
     rc = enc(&plan->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(in), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {  // S layout: [P][G][2][lh][8] as {64, lh/8 lines, 2 parities, G, P}
     const cuuint64_t lh = static_cast<cuuint64_t>(lh_S(lin));
-    const cuuint64_t dims[5] = {64, lh / 8, 2, G, static_cast<cuuint64_t>(P)};
-    const cuuint64_t strides[4] = {128, lh * 16, 2 * lh * 16, G * 2 * lh * 16};
+    const cuuint64_t dims[5] = {64, lh / 8, 2, CG, static_cast<cuuint64_t>(P)};
+    const cuuint64_t strides[4] = {128, lh * 16, 2 * lh * 16, CG * 2 * lh * 16};
     const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(a.rows / 8), 1, static_cast<cuuint32_t>(a.ck / 8), 1};
     rc = enc(&plan->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(in), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -620,8 +687,17 @@ cudaError_t init_conv_kernel() {
 }
 
 cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st) {
-  conv_tc_kernel<<<plan.grid, kConvThreads, plan.smem_bytes, st>>>(plan.tmap, plan.args);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.grid);
+  cfg.blockDim = dim3(kConvThreads);
+  cfg.dynamicSmemBytes = plan.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel, plan.tmap, plan.args);
 }
 
 }  // namespace hb

@@ -48,6 +48,20 @@ std::vector<LayerSpec> member_layers(int width, int depth, int window) {
   return v;
 }
 
+struct Group {
+  int width = 0, depth = 0, lead_any = 0, lane = 0;
+  std::vector<int> mi;                 // positions in hb_ctx::selected (zoo order)
+  std::vector<LayerSpec> layers;
+  std::vector<StemMember> stem;        // per member: its lead's normalised windows, stem weights
+  std::vector<uint8_t*> wpack;         // per conv layer: [G][member image]
+  std::vector<float*> bias;            // per conv layer: [G][bias_len]
+  float* fc_w = nullptr;               // [G][c_last]
+  float* head_partial = nullptr;       // [G*P][mt]
+  int head_mt = 0;
+  double flops = 0;
+  size_t plan0 = 0;                    // first plan index
+};
+
 struct Member {
   int idx = -1, lead = 0, width = 0, depth = 0;
   std::vector<LayerSpec> layers;
@@ -57,7 +71,6 @@ struct Member {
   std::vector<float*> bias;
   float* fc_w = nullptr;
   float fc_b = 0.f;
-  float* head_partial = nullptr;  // [P][mt]
   int head_mt = 0;
   double flops = 0, bytes = 0;
 };
@@ -67,6 +80,7 @@ struct Member {
 struct hb_ctx {
   int device = 0, P = 0, leads = 0, fs = 0, W = 0, hop = 0, R = 0, keep = 0, num_sms = 148;
   int max_lanes = 4;  // concurrent member branches in the tick graph (HB_LANES overrides)
+  int group_off = 0;  // HB_NO_GROUP=1: one launch per member and layer (A/B experiments)
   cudaStream_t own = nullptr;
   float* ring = nullptr;
   float* staged = nullptr;   // [P][leads][hop]
@@ -77,11 +91,13 @@ struct hb_ctx {
   float* stats = nullptr;    // [P][leads][2]
   std::map<int, Member> members;
   std::vector<int> selected;
-  // per-selection resources: `lanes` concurrent member branches, 3 rotating
-  // activation buffers each (members on one branch run back to back)
+  // per-selection resources: selected members of identical architecture form
+  // a group that runs as ONE launch per layer (activations G*P patients deep);
+  // groups are spread over `lanes` concurrent graph branches, 3 rotating
+  // activation buffers per lane (groups on one branch run back to back)
   int lanes = 1;
   std::vector<__half*> act;
-  std::vector<int> member_lane;
+  std::vector<Group> groups;
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> ev;
   size_t act_bytes = 0;
@@ -118,11 +134,17 @@ void free_selection(hb_ctx* c) {
   c->graph = nullptr;
   for (auto& a : c->act) cudaFree(a);
   c->act.clear();
+  for (auto& g : c->groups) {
+    for (auto p : g.wpack) cudaFree(p);
+    for (auto p : g.bias) cudaFree(p);
+    cudaFree(g.fc_w);
+    cudaFree(g.head_partial);
+  }
+  c->groups.clear();
   for (auto s2 : c->side) cudaStreamDestroy(s2);
   c->side.clear();
   for (auto e : c->ev) cudaEventDestroy(e);
   c->ev.clear();
-  c->member_lane.clear();
   c->act_bytes = 0;
   if (c->d_heads) cudaFree(c->d_heads);
   if (c->member_logits) cudaFree(c->member_logits);
@@ -140,7 +162,6 @@ void free_member(Member& m) {
   for (auto p : m.wpack) cudaFree(p);
   for (auto p : m.bias) cudaFree(p);
   cudaFree(m.fc_w);
-  cudaFree(m.head_partial);
 }
 
 // Kernel kinds reported by hb_profile_tick.
@@ -176,27 +197,32 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   // stay clean.
   const bool fork = (pr->ev == nullptr) && c->lanes > 1;
   if (fork) CK(c, cudaEventRecord(c->ev[0], st));
-  size_t pi = 0;
-  for (size_t mi = 0; mi < c->selected.size(); ++mi) {
-    Member& m = c->members[c->selected[mi]];
-    const int ln = c->member_lane[mi];
+  std::vector<bool> lane_started(c->lanes, false);
+  for (const Group& g : c->groups) {
+    const int ln = g.lane;
     cudaStream_t ms = fork ? c->side[ln] : st;
-    if (fork && mi < static_cast<size_t>(c->lanes)) CK(c, cudaStreamWaitEvent(ms, c->ev[0], 0));
+    if (fork && !lane_started[ln]) {
+      CK(c, cudaStreamWaitEvent(ms, c->ev[0], 0));
+      lane_started[ln] = true;
+    }
     __half* const* act = &c->act[3 * ln];
-    const LayerSpec& s0 = m.layers[0];
-    CK(c, launch_stem(c->xn + static_cast<size_t>(m.lead) * c->P * c->W, c->W, c->P, c->W,
-                      round_up(s0.lout, 8), s0.cout, s0.pad, m.stem_w, m.stem_b, act[0], ms));
-    pr->mark(ms, K_STEM, P * 2.0 * s0.cout * kTaps * s0.lout, P * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
-    for (size_t li = 1; li < m.layers.size(); ++li) {
-      const LayerSpec& L = m.layers[li];
+    const int G = static_cast<int>(g.mi.size());
+    const double rows = P * G;
+    const LayerSpec& s0 = g.layers[0];
+    CK(c, launch_stem(g.stem.data(), G, c->W, c->P, c->W, round_up(s0.lout, 8), s0.cout, s0.pad, act[0], ms));
+    pr->mark(ms, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+    size_t pi = g.plan0;
+    for (size_t li = 1; li < g.layers.size(); ++li) {
+      const LayerSpec& L = g.layers[li];
       CK(c, launch_conv(c->plans[pi++], ms));
-      pr->mark(ms, K_CONV, P * 2.0 * L.cin * L.cout * kTaps * L.lout,
-               P * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
-                          (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
+      pr->mark(ms, K_CONV, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
+               rows * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
+                             (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
     }
   }
   if (fork) {
     for (int ln = 0; ln < c->lanes; ++ln) {
+      if (!lane_started[ln]) continue;
       CK(c, cudaEventRecord(c->ev[1 + ln], c->side[ln]));
       CK(c, cudaStreamWaitEvent(st, c->ev[1 + ln], 0));
     }
@@ -213,28 +239,50 @@ int build_selection(hb_ctx* c) {
   if (!c->dirty) return HB_OK;
   free_selection(c);
   if (c->selected.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
-  // activation buffers sized for the largest layer output of any selected member
   const int M = static_cast<int>(c->selected.size());
-  c->lanes = std::max(1, std::min(M, c->max_lanes));
-  size_t need = 0;
-  for (int idx : c->selected)
-    for (auto& L : c->members[idx].layers)
-      need = std::max(need, static_cast<size_t>(c->P) * L.cout * act_rows(L.lout, 1) * sizeof(__half));
-  c->act.assign(3 * c->lanes, nullptr);
-  for (auto& a : c->act) {
-    CK(c, cudaMalloc(&a, need));
-    CK(c, cudaMemset(a, 0, need));
+  // group selected members by architecture (first-occurrence order; <= kMaxGroup per group)
+  for (int mi = 0; mi < M; ++mi) {
+    const Member& m = c->members[c->selected[mi]];
+    Group* gp = nullptr;
+    if (!c->group_off)
+      for (auto& g : c->groups)
+        if (g.width == m.width && g.depth == m.depth && static_cast<int>(g.mi.size()) < kMaxGroup) gp = &g;
+    if (!gp) {
+      c->groups.emplace_back();
+      gp = &c->groups.back();
+      gp->width = m.width;
+      gp->depth = m.depth;
+      gp->layers = m.layers;
+    }
+    gp->mi.push_back(mi);
+    gp->flops += m.flops;
   }
-  c->act_bytes = need;
-  // greedy FLOP balance of members over lanes (zoo order kept within a lane)
-  {
+  c->lanes = std::max(1, std::min(static_cast<int>(c->groups.size()), c->max_lanes));
+  {  // greedy FLOP balance of groups over lanes, largest first
+    std::vector<size_t> order(c->groups.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t a, size_t b) { return c->groups[a].flops > c->groups[b].flops; });
     std::vector<double> load(c->lanes, 0.0);
-    for (int idx : c->selected) {
+    for (size_t i : order) {
       const int ln = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-      c->member_lane.push_back(ln);
-      load[ln] += c->members[idx].flops;
+      c->groups[i].lane = ln;
+      load[ln] += c->groups[i].flops;
     }
   }
+  // activation buffers per lane, sized for the largest layer of its groups
+  std::vector<size_t> need(c->lanes, 0);
+  for (auto& g : c->groups)
+    for (auto& L : g.layers)
+      need[g.lane] = std::max(need[g.lane], static_cast<size_t>(c->P) * g.mi.size() * L.cout *
+                                                act_rows(L.lout, 1) * sizeof(__half));
+  c->act.assign(3 * c->lanes, nullptr);
+  for (int ln = 0; ln < c->lanes; ++ln)
+    for (int k = 0; k < 3; ++k) {
+      CK(c, cudaMalloc(&c->act[3 * ln + k], need[ln]));
+      CK(c, cudaMemset(c->act[3 * ln + k], 0, need[ln]));
+      c->act_bytes += need[ln];
+    }
   c->side.resize(c->lanes);
   for (auto& s2 : c->side) CK(c, cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
   c->ev.resize(1 + c->lanes);
@@ -243,14 +291,42 @@ int build_selection(hb_ctx* c) {
   CK(c, cudaMalloc(&c->ens_prob, sizeof(float) * c->P));
   CK(c, cudaMalloc(&c->ens_logit, sizeof(float) * c->P));
   CK(c, cudaMalloc(&c->ens_sums, sizeof(float) * 2 * c->P));
-  std::vector<HeadMember> heads;
-  for (size_t mi = 0; mi < c->selected.size(); ++mi) {
-    Member& m = c->members[c->selected[mi]];
-    __half* const* act = &c->act[3 * c->member_lane[mi]];
+  std::vector<HeadMember> heads(M);
+  for (auto& g : c->groups) {
+    const int G = static_cast<int>(g.mi.size());
+    const int c_last = g.layers.back().cout;
+    // group-contiguous weight images (device-to-device from the registered members)
+    for (size_t li = 1; li < g.layers.size(); ++li) {
+      const LayerSpec& L = g.layers[li];
+      const size_t wb = wpack_bytes(L.cin, L.cout), bl = bias_len(L.cout);
+      uint8_t* w;
+      float* b;
+      CK(c, cudaMalloc(&w, wb * G));
+      CK(c, cudaMalloc(&b, sizeof(float) * bl * G));
+      for (int k = 0; k < G; ++k) {
+        const Member& m = c->members[c->selected[g.mi[k]]];
+        CK(c, cudaMemcpy(w + wb * k, m.wpack[li - 1], wb, cudaMemcpyDeviceToDevice));
+        CK(c, cudaMemcpy(b + bl * k, m.bias[li - 1], sizeof(float) * bl, cudaMemcpyDeviceToDevice));
+      }
+      g.wpack.push_back(w);
+      g.bias.push_back(b);
+    }
+    CK(c, cudaMalloc(&g.fc_w, sizeof(float) * c_last * G));
+    g.head_mt = (g.layers.back().lout + kBM - 1) / kBM;
+    CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P * g.head_mt));
+    for (int k = 0; k < G; ++k) {
+      const Member& m = c->members[c->selected[g.mi[k]]];
+      CK(c, cudaMemcpy(g.fc_w + c_last * k, m.fc_w, sizeof(float) * c_last, cudaMemcpyDeviceToDevice));
+      g.stem.push_back({c->xn + static_cast<size_t>(m.lead) * c->P * c->W, m.stem_w, m.stem_b});
+      heads[g.mi[k]] = {g.head_partial + static_cast<size_t>(k) * c->P * g.head_mt, g.head_mt,
+                        1.f / static_cast<float>(g.layers.back().lout), m.fc_b};
+    }
+    __half* const* act = &c->act[3 * g.lane];
+    g.plan0 = c->plans.size();
     int cur = 0;
-    const int nblocks = static_cast<int>(m.layers.size() - 1) / 2;
-    for (size_t li = 1; li < m.layers.size(); ++li) {
-      const LayerSpec& L = m.layers[li];
+    const int nblocks = static_cast<int>(g.layers.size() - 1) / 2;
+    for (size_t li = 1; li < g.layers.size(); ++li) {
+      const LayerSpec& L = g.layers[li];
       const bool conv1 = (li % 2 == 1);
       const int blk = static_cast<int>(li - 1) / 2;
       int src = cur, dst, out_split = 0, res_len = 0;
@@ -261,20 +337,19 @@ int build_selection(hb_ctx* c) {
         src = (cur + 1) % 3;
         dst = (cur + 2) % 3;
         res = act[cur];
-        res_len = m.layers[li - 1].lin;
+        res_len = g.layers[li - 1].lin;
         // the output of an even block feeds the next (stride-2) block: parity-split layout
         out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
       }
       ConvPlan plan;
-      const char* e = plan_conv(&plan, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
-                                L.head ? nullptr : act[dst], out_split, m.wpack[li - 1], m.bias[li - 1], res,
-                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? m.fc_w : nullptr,
-                                L.head ? m.head_partial : nullptr, c->num_sms);
+      const char* e = plan_conv(&plan, G, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+                                L.head ? nullptr : act[dst], out_split, g.wpack[li - 1], g.bias[li - 1], res,
+                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr,
+                                L.head ? g.head_partial : nullptr, c->num_sms);
       if (e) return fail(c, HB_E_INVALID, e);
       c->plans.push_back(plan);
       if (!conv1) cur = dst;
     }
-    heads.push_back({m.head_partial, m.head_mt, 1.f / static_cast<float>(m.layers.back().lout), m.fc_b});
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
   CK(c, cudaMemcpy(c->d_heads, heads.data(), sizeof(HeadMember) * heads.size(), cudaMemcpyHostToDevice));
@@ -327,6 +402,7 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   c->R = cfg->ring_len > 0 ? cfg->ring_len : round_up(cfg->window_len + cfg->hop, 256);
   c->keep = cfg->keep_windows;
   if (getenv("HB_LANES")) c->max_lanes = std::max(1, atoi(getenv("HB_LANES")));
+  if (getenv("HB_NO_GROUP")) c->group_off = atoi(getenv("HB_NO_GROUP"));
   if (c->R < c->W) {
     delete c;
     return fail(nullptr, HB_E_CONFIG, "ring_len must be >= window_len");
@@ -425,7 +501,6 @@ int hb_add_member(hb_ctx* c, int idx, int lead, int width, int depth, const floa
   p += c_last;
   m.fc_b = *p;
   m.head_mt = (m.layers.back().lout + kBM - 1) / kBM;
-  CK(c, cudaMalloc(&m.head_partial, sizeof(float) * c->P * m.head_mt));
   for (auto& L : m.layers) {
     m.flops += 2.0 * L.cin * L.cout * kTaps * L.lout;
     m.bytes += 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout));
@@ -680,7 +755,7 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
     CK(none, cudaMemcpy(dfc, fc_w_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
   }
   ConvPlan plan;
-  const char* e = plan_conv(&plan, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
+  const char* e = plan_conv(&plan, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
                             static_cast<__half*>(out), out_split, dw, db, static_cast<const __half*>(res), res_mode,
                             res_c, res_len > 0 ? res_len : lout, dfc, head_out, sms);
   int rc = HB_OK;
@@ -727,7 +802,7 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
   CK(none, cudaMalloc(&db, nbias * 4));
   CK(none, cudaMemset(db, 0, nbias * 4));
   ConvPlan plan;
-  const char* e = plan_conv(&plan, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
+  const char* e = plan_conv(&plan, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
                             static_cast<__half*>(dout), 0, static_cast<uint8_t*>(dw), static_cast<float*>(db),
                             res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
                             res_mode == 2 ? 2 * lin : lout, nullptr, nullptr, sms);
@@ -793,8 +868,8 @@ int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b
   CK(none, cudaMemcpy(dw, w_host, sizeof(float) * cout * kTaps, cudaMemcpyHostToDevice));
   CK(none, cudaMalloc(&db, sizeof(float) * cout));
   CK(none, cudaMemcpy(db, b_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
-  cudaError_t ce = launch_stem(static_cast<const __half*>(xn), L, P, L, round_up(L, 8), cout, tot / 2, dw, db,
-                               static_cast<__half*>(out), st);
+  const StemMember sm{static_cast<const __half*>(xn), dw, db};
+  cudaError_t ce = launch_stem(&sm, 1, L, P, L, round_up(L, 8), cout, tot / 2, static_cast<__half*>(out), st);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
   cudaFree(dw);
   cudaFree(db);

@@ -9,6 +9,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 
 namespace hb {
 
@@ -32,7 +33,8 @@ inline int lh_S(int L) { return round_up((L + 1) / 2, 8); }
 inline int act_rows(int L, int split) { return split ? 2 * lh_S(L) : lp_I(L); }
 
 struct ConvArgs {
-  int P, cin, cout, bn, n_ntiles;  // bn = per-tile N (mult of 16, <=256)
+  int P, cin, cout, bn, n_ntiles;  // P = G*Pm rows of the activation tensors; bn = per-tile N (mult of 16, <=256)
+  int G, Pm;                       // members sharing this layer shape (one launch), patients per member
   int lin, lout;
   int out_split, out_lp, out_lh;   // output layout (I: out_lp rows; S: 2 x out_lh rows)
   int out_rows;                    // positions that must be written (valid or zero padding)
@@ -42,14 +44,16 @@ struct ConvArgs {
   uint32_t a_stage_bytes, b_chunk_bytes;
   int na_stages, nb_slots, b_resident;
   uint32_t tmem_cols;
-  const uint8_t* wpack;            // [ntile][kchunk][kstep][2][bn][16 B] fp16
-  const float* bias;               // [n_ntiles*bn] (zero padded)
+  const uint8_t* wpack;            // [G][ntile][kchunk][kstep][2][bn][16 B] fp16
+  size_t wpack_stride;             // bytes per member
+  const float* bias;               // [G][n_ntiles*bn] (zero padded)
+  int bias_stride;                 // floats per member
   __half* out;                     // output activation (layout out_split)
   const __half* res;               // shortcut source or null
   int res_mode;                    // 0 none, 1 identity (I layout), 2 maxpool(2) (S layout)
   int res_c, res_rows;             // shortcut channels; plane rows (I: lp, S: lh)
   int relu;
-  const float* fc_w;               // head: [cout] -> head_out[P][mt_per_p] (null = no head)
+  const float* fc_w;               // head: [G][cout] -> head_out[G*Pm][mt_per_p] (null = no head)
   float* head_out;
   int dbg;                         // experiments only (HB_DEBUG env)
   unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]
@@ -65,10 +69,30 @@ struct ConvPlan {
 // Build a plan (tensor map + tiling) for one conv layer.  The input layout is
 // I for stride 1 and S for stride 2; res (if any) is I for identity, S for
 // maxpool; `out_split` selects the output layout.  Returns 0 or an error string.
-const char* plan_conv(ConvPlan* plan, int P, int cin, int cout, int lin, int lout, int stride, int pad,
+// G members of identical layer shape run in one launch: activations are
+// [G*Pm] patients deep, weights / bias / fc are G consecutive per-member images.
+const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                       const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
                       const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
                       float* head_out, int num_sms);
+size_t bias_len(int cout);  // per-member bias floats (zero padded to whole N tiles)
+// Programmatic dependent launch on/off (HB_NO_PDL=1 disables).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 // Host-side packing of canonical weights W[cout][cin][16] into the plan's B image.
 size_t wpack_bytes(int cin, int cout);
 void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */);
@@ -82,9 +106,17 @@ inline cudaError_t init_kernels() {
   return e != cudaSuccess ? e : init_stream_kernels();
 }
 
-// stem conv (C_in = 1) + bias + ReLU on CUDA cores: xn[p][L] fp16 -> NG8 out.
-cudaError_t launch_stem(const __half* xn, int x_stride, int P, int L, int lp_out, int cout, int pad,
-                        const float* w /*[cout][16]*/, const float* b, __half* out, cudaStream_t st);
+// stem conv (C_in = 1) + bias + ReLU on CUDA cores for G members of one
+// group: member g reads xn + x_off[g] ([Pm][L] fp16), weights w[g][cout][16],
+// b[g][cout]; writes rows [g*Pm, (g+1)*Pm) of the NG8 output.
+struct StemMember {
+  const __half* x;  // [Pm][x_stride]
+  const float* w;   // [cout][16]
+  const float* b;   // [cout]
+};
+constexpr int kMaxGroup = 16;
+cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int G, int x_stride, int Pm, int L,
+                        int lp_out, int cout, int pad, __half* out, cudaStream_t st);
 
 // K1+K2: ring append of `n_new` samples per stream at the device write cursor
 // *wpos, then (if xn != null) gather of the window ending at *wpos + n_new and

@@ -10,12 +10,13 @@
 //         members in zoo order, normalised by popcount; it also emits the mean
 //         of member sigmoids (north star).  Fixed order, no float atomics.
 #include "hb_kernels.cuh"
+#include "hb_ptx.cuh"
 
 #include <cstdint>
 
 namespace hb {
 
-constexpr int kWinThreads = 256;
+constexpr int kWinThreads = 1024;
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
 #pragma unroll
@@ -45,21 +46,33 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   __shared__ float red[33];
   const int s = blockIdx.x;  // stream = p*leads + lead
   const int p = s / leads, lead = s % leads;
+  pdl_wait();  // the ring cursor / rings / staging buffer belong to the previous tick's chain
+  pdl_trigger();
   const long long wpos = *wpos_p;
   float* rs = ring + static_cast<size_t>(s) * R;
   const float* src = staged + static_cast<size_t>(s) * n_new;
-  for (int i = threadIdx.x; i < n_new; i += blockDim.x) rs[(wpos + i) % R] = src[i];
-  if (xn == nullptr) return;
-  __syncthreads();
-  // window = samples [end - W, end) with end = wpos + n_new
-  const long long start = wpos + n_new - W;
-  float part = 0.f;
-  for (int i = threadIdx.x; i < W; i += blockDim.x) {
-    const long long n = start + i;
-    const float v = (n >= 0) ? rs[n % R] : 0.f;
-    win[i] = v;
-    part += v;
+  const int w0 = static_cast<int>(wpos % R);
+  for (int i = threadIdx.x; i < n_new; i += blockDim.x) {
+    const float v = src[i];
+    int j = w0 + i;
+    if (j >= R) j -= R;
+    rs[j] = v;
+    if (xn != nullptr && i >= n_new - W) win[W - n_new + i] = v;  // newest samples straight from staging
   }
+  if (xn == nullptr) return;
+  // window = samples [end - W, end) with end = wpos + n_new; the part older
+  // than this tick's append comes from the ring (written by earlier ticks)
+  const long long start = wpos + n_new - W;
+  const int old_n = W > n_new ? W - n_new : 0;
+  int r0 = static_cast<int>(((start % R) + R) % R);
+  for (int i = threadIdx.x; i < old_n; i += blockDim.x) {
+    int j = r0 + i;
+    if (j >= R) j -= R;
+    win[i] = (start + i >= 0) ? rs[j] : 0.f;
+  }
+  __syncthreads();
+  float part = 0.f;
+  for (int i = threadIdx.x; i < W; i += blockDim.x) part += win[i];
   const float mean = block_sum(part, red) / static_cast<float>(W);
   float sq = 0.f;
   for (int i = threadIdx.x; i < W; i += blockDim.x) {
@@ -70,7 +83,13 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   const float sd = sqrtf(var);
   const float rstd = 1.f / fmaxf(sd, 1e-6f);
   __half* dst = xn + (static_cast<size_t>(lead) * P + p) * W;
-  for (int i = threadIdx.x; i < W; i += blockDim.x) dst[i] = __float2half_rn((win[i] - mean) * rstd);
+  if ((W & 1) == 0) {
+    __half2* d2 = reinterpret_cast<__half2*>(dst);
+    for (int i = threadIdx.x; i < W / 2; i += blockDim.x)
+      d2[i] = __floats2half2_rn((win[2 * i] - mean) * rstd, (win[2 * i + 1] - mean) * rstd);
+  } else {
+    for (int i = threadIdx.x; i < W; i += blockDim.x) dst[i] = __float2half_rn((win[i] - mean) * rstd);
+  }
   if (raw_out) {
     float* r = raw_out + static_cast<size_t>(s) * W;
     for (int i = threadIdx.x; i < W; i += blockDim.x) r[i] = win[i];
@@ -81,15 +100,17 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   }
 }
 
-__global__ void advance_kernel(long long* wpos, int n) { *wpos += n; }
+__global__ void advance_kernel(long long* wpos, int n) {
+  pdl_wait();
+  *wpos += n;
+}
 
 cudaError_t launch_ingest_window(const float* staged, float* ring, const long long* wpos, int P, int leads,
                                  int n_new, int R, int window, __half* xn, float* raw_out, float* stats,
                                  cudaStream_t st) {
   const size_t smem = xn ? static_cast<size_t>(window) * sizeof(float) : 0;
-  ingest_window_kernel<<<P * leads, kWinThreads, smem, st>>>(staged, ring, wpos, P, leads, n_new, R, window, xn,
-                                                             raw_out, stats);
-  return cudaGetLastError();
+  return launch_pdl(ingest_window_kernel, dim3(P * leads), dim3(kWinThreads), smem, st, staged, ring, wpos, P, leads,
+                    n_new, R, window, xn, raw_out, stats);
 }
 
 cudaError_t init_stream_kernels() {
@@ -97,60 +118,97 @@ cudaError_t init_stream_kernels() {
 }
 
 cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st) {
-  advance_kernel<<<1, 1, 0, st>>>(wpos, n);
-  return cudaGetLastError();
+  return launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, wpos, n);
 }
 
 // ------------------------------------------------------------------ K3 stem
 // out[p][g][l][8] = ReLU(b + sum_t w[c][t] * x[p][l + t - pad]),  rows [L, Lp) = 0.
-constexpr int kStemTile = 256;
-__global__ void __launch_bounds__(kStemTile) stem_kernel(const __half* __restrict__ xn, int x_stride, int L,
-                                                         int lp_out, int cout, int pad,
-                                                         const float* __restrict__ w,
-                                                         const float* __restrict__ b, __half* __restrict__ out) {
+// One CTA = 1024 positions of one (member, patient) row; each thread owns 4
+// consecutive positions (19 samples in registers) and walks the channels
+// 8 at a time, weights broadcast from shared memory as float4.  The output
+// rows of one 8-channel plane are written as 4 x 16 B per thread (a warp
+// writes 2 KB contiguous).
+constexpr int kStemThreads = 256;
+constexpr int kStemPos = 4;
+constexpr int kStemTile = kStemThreads * kStemPos;
+struct StemArgs {
+  StemMember m[kMaxGroup];
+  int Pm, x_stride, L, lp_out, cout, pad;
+  __half* out;
+};
+
+__global__ void __launch_bounds__(kStemThreads) stem_kernel(const __grid_constant__ StemArgs a) {
   __shared__ float sx[kStemTile + kTaps];
-  __shared__ float sw[128 * kTaps];
+  __shared__ __align__(16) float sw[128 * kTaps];
   __shared__ float sb[128];
-  const int p = blockIdx.y;
+  const int row = blockIdx.y;            // g * Pm + p
+  const int g = row / a.Pm, p = row - g * a.Pm;
   const int l0 = blockIdx.x * kStemTile;
-  const __half* x = xn + static_cast<size_t>(p) * x_stride;
-  for (int i = threadIdx.x; i < kStemTile + kTaps; i += blockDim.x) {
-    const int pos = l0 + i - pad;
-    sx[i] = (pos >= 0 && pos < L) ? __half2float(x[pos]) : 0.f;
+  const StemMember& mb = a.m[g];
+  for (int i = threadIdx.x; i < a.cout * kTaps; i += kStemThreads) sw[i] = mb.w[i];
+  for (int i = threadIdx.x; i < a.cout; i += kStemThreads) sb[i] = mb.b[i];
+  pdl_wait();   // x is the window kernel's output
+  pdl_trigger();
+  const __half* x = mb.x + static_cast<size_t>(p) * a.x_stride;
+  for (int i = threadIdx.x; i < kStemTile + kTaps; i += kStemThreads) {
+    const int pos = l0 + i - a.pad;
+    sx[i] = (pos >= 0 && pos < a.L) ? __half2float(x[pos]) : 0.f;
   }
-  for (int i = threadIdx.x; i < cout * kTaps; i += blockDim.x) sw[i] = w[i];
-  for (int i = threadIdx.x; i < cout; i += blockDim.x) sb[i] = b[i];
   __syncthreads();
-  const int l = l0 + threadIdx.x;
-  if (l >= lp_out) return;
-  float xv[kTaps];
+  const int lt = threadIdx.x * kStemPos;
+  const int l = l0 + lt;
+  if (l >= a.lp_out) return;
+  float xv[kStemPos + kTaps - 1];
 #pragma unroll
-  for (int t = 0; t < kTaps; ++t) xv[t] = sx[threadIdx.x + t];
-  const bool valid = l < L;
-  const int G = cout / 8;
-  for (int g = 0; g < G; ++g) {
-    uint4 pk;
-    __half2* o2 = reinterpret_cast<__half2*>(&pk);
+  for (int t = 0; t < kStemPos + kTaps - 1; ++t) xv[t] = sx[lt + t];
+  const int G8 = a.cout / 8;
+  __half* orow = a.out + static_cast<size_t>(row) * G8 * a.lp_out * 8;
+  for (int g8 = 0; g8 < G8; ++g8) {
+    float acc[kStemPos][8];
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      float a0 = sb[g * 8 + j], a1 = sb[g * 8 + j + 1];
+    for (int j = 0; j < 8; ++j) {
+      const float bj = sb[g8 * 8 + j];
 #pragma unroll
-      for (int t = 0; t < kTaps; ++t) {
-        a0 = fmaf(sw[(g * 8 + j) * kTaps + t], xv[t], a0);
-        a1 = fmaf(sw[(g * 8 + j + 1) * kTaps + t], xv[t], a1);
+      for (int q = 0; q < kStemPos; ++q) acc[q][j] = bj;
+      const float4* wj = reinterpret_cast<const float4*>(sw + (g8 * 8 + j) * kTaps);
+#pragma unroll
+      for (int t4 = 0; t4 < kTaps / 4; ++t4) {
+        const float4 w4 = wj[t4];
+        const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < kStemPos; ++q) acc[q][j] = fmaf(wv[u], xv[q + 4 * t4 + u], acc[q][j]);
       }
-      o2[j / 2] = valid ? __floats2half2_rn(fmaxf(a0, 0.f), fmaxf(a1, 0.f)) : __floats2half2_rn(0.f, 0.f);
     }
-    *reinterpret_cast<uint4*>(out + ((static_cast<size_t>(p) * G + g) * lp_out + l) * 8) = pk;
+#pragma unroll
+    for (int q = 0; q < kStemPos; ++q) {
+      if (l + q >= a.lp_out) break;
+      const bool valid = l + q < a.L;
+      uint4 pk;
+      __half2* o2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+      for (int j = 0; j < 8; j += 2)
+        o2[j / 2] = valid ? __floats2half2_rn(fmaxf(acc[q][j], 0.f), fmaxf(acc[q][j + 1], 0.f))
+                          : __floats2half2_rn(0.f, 0.f);
+      *reinterpret_cast<uint4*>(orow + (static_cast<size_t>(g8) * a.lp_out + l + q) * 8) = pk;
+    }
   }
 }
 
-cudaError_t launch_stem(const __half* xn, int x_stride, int P, int L, int lp_out, int cout, int pad, const float* w,
-                        const float* b, __half* out, cudaStream_t st) {
-  if (cout > 128 || cout % 8) return cudaErrorInvalidValue;
-  dim3 grid((lp_out + kStemTile - 1) / kStemTile, P);
-  stem_kernel<<<grid, kStemTile, 0, st>>>(xn, x_stride, L, lp_out, cout, pad, w, b, out);
-  return cudaGetLastError();
+cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int lp_out, int cout, int pad,
+                        __half* out, cudaStream_t st) {
+  if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup) return cudaErrorInvalidValue;
+  StemArgs a;
+  for (int g = 0; g < G; ++g) a.m[g] = members[g];
+  a.Pm = Pm;
+  a.x_stride = x_stride;
+  a.L = L;
+  a.lp_out = lp_out;
+  a.cout = cout;
+  a.pad = pad;
+  a.out = out;
+  return launch_pdl(stem_kernel, dim3((lp_out + kStemTile - 1) / kStemTile, G * Pm), dim3(kStemThreads), 0, st, a);
 }
 
 // ------------------------------------------------------------------ K5 aggregate
@@ -164,6 +222,8 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __rest
                                                         float* __restrict__ ens_sums) {
   __shared__ float s_logit[kMaxMembers];
   const int p = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m = warp; m < M; m += 8) {
     const HeadMember hm = mem[m];
@@ -192,8 +252,8 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __rest
 cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits, float* ens_prob,
                              float* ens_logit, float* ens_sums, cudaStream_t st) {
   if (M < 1 || M > kMaxMembers) return cudaErrorInvalidValue;
-  aggregate_kernel<<<P, 256, 0, st>>>(members_dev, M, P, member_logits, ens_prob, ens_logit, ens_sums);
-  return cudaGetLastError();
+  return launch_pdl(aggregate_kernel, dim3(P), dim3(256), 0, st, members_dev, M, P, member_logits, ens_prob,
+                    ens_logit, ens_sums);
 }
 
 // Member-sharded finish: sums[2][P] reduced over ranks -> means over the total popcount.

@@ -138,6 +138,10 @@ class MemberShardedEngine:
         self.patients = patients
         mine = Selector.from_indices(zoo.n, self.bins[rank])
         self.engine = EnsembleEngine(zoo, mine, patients, **engine_kw)
+        import torch
+        # a real (non-legacy) stream: the library treats handle 0 as "its own
+        # stream", which does not order with torch's legacy default stream
+        self.stream = torch.cuda.Stream()
 
     def _sums_tensor(self):
         import torch
@@ -149,11 +153,13 @@ class MemberShardedEngine:
         """Every rank passes ALL beds' samples [P, leads, hop]; rank 0 gets (prob, logit) device tensors."""
         import torch
         a = np.ascontiguousarray(samples_all, dtype=np.float32)
-        staged = torch.from_numpy(a).cuda(non_blocking=False)
-        stream = torch.cuda.current_stream().cuda_stream
-        self.engine.stage_device(staged.data_ptr(), stream)
-        self.engine.tick_device(stream)
-        return combine_member_sums(self._sums_tensor(), self.m_total, self.group)
+        with torch.cuda.stream(self.stream):
+            staged = torch.from_numpy(a).cuda(non_blocking=False)
+            self.engine.stage_device(staged.data_ptr(), self.stream.cuda_stream)
+            self.engine.tick_device(self.stream.cuda_stream)
+            out = combine_member_sums(self._sums_tensor(), self.m_total, self.group)
+        self.stream.synchronize()
+        return out
 
     def close(self):
         self.engine.close()
