@@ -15,7 +15,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libholmes_b200.so")
+LIB_PATH = os.environ.get("HB_LIB_PATH") or os.path.join(_HERE, "libholmes_b200.so")  # override: A/B experiments
 
 HB_OK, HB_E_INVALID, HB_E_CONFIG, HB_E_EMPTY, HB_E_CUDA, HB_E_STATE, HB_E_METRIC = range(7)
 
@@ -87,6 +87,8 @@ def lib() -> C.CDLL:
                     "(there is no CPU fallback)")
             handle = C.CDLL(LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("HB_LIB_PATH") and not hasattr(handle, name):
+                    continue  # an older library under A/B test
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args

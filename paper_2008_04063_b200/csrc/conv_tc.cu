@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [2][4] per-warp head partials
-  float* s_bias = s_head + 8;                                  // [bn]
-  float* s_fc = s_bias + 256;                                  // [bn]
+  float* s_bias = s_head + 8;                                  // [G][bn] when every N tile is whole
+  float* s_fc = s_bias + a.sb_len;                             // [G][bn]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -100,10 +100,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
-  const bool uniform_bias = (a.n_ntiles == 1 && a.G == 1);  // bias / fc cached in smem
-  for (int i = threadIdx.x; i < a.bn; i += blockDim.x) {
-    s_bias[i] = uniform_bias ? a.bias[i] : 0.f;
-    s_fc[i] = (a.fc_w && uniform_bias) ? a.fc_w[i < a.cout ? i : 0] : 0.f;
+  const bool smem_bias = a.sb_len > 0;  // every member's bias / fc cached in smem
+  if (smem_bias) {
+    for (int i = threadIdx.x; i < a.G * a.bn; i += blockDim.x) {
+      const int g = i / a.bn, c = i - g * a.bn;
+      s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + c];
+      s_fc[i] = a.fc_w ? a.fc_w[static_cast<size_t>(g) * a.cout + (c < a.cout ? c : 0)] : 0.f;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -140,21 +143,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         loaded_key = t0.g * a.n_ntiles + t0.nt;
       }
       pdl_wait();
-      int li = 0;  // local tile count
+      int li = 0;       // local tile count
+      int reloads = 0;  // resident-B reloads so far
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++li) {
         const TileIdx t = decode_tile(a, tile);
         const int p = t.p;
         const int blk = (t.mt * kBM + a.row0) / 8;  // first 128-B line (8 rows)
         const int key = t.g * a.n_ntiles + t.nt;
         const bool load_b = !a.b_resident || key != loaded_key;
-        // Reloading resident weights (next member of the group): the previous
-        // tile's MMAs must have drained out of the B slots first.
-        if (a.b_resident && load_b && li > 0) mbar_wait(&acc_full[(li - 1) & 1], ((li - 1) >> 1) & 1);
+        // Reloading resident weights (next member of the group): the MMA warp
+        // signals b_empty[0] once per reload, after the last MMA that reads
+        // the old weights has completed (one completion per reload, so the
+        // phase parity is unambiguous).
+        if (a.b_resident && load_b && li > 0) mbar_wait(&b_empty[0], static_cast<uint32_t>(reloads++) & 1u, 1);
         loaded_key = key;
         for (int kc = 0; kc < a.n_kchunks; ++kc) {
           if (load_b) {
             const int slot = a.b_resident ? kc : bs;
-            if (!a.b_resident) mbar_wait(&b_empty[bs], bph ^ 1);
+            if (!a.b_resident) mbar_wait(&b_empty[bs], bph ^ 1, 2);
             mbar_arrive_expect_tx(&b_full[slot], a.b_chunk_bytes);
             bulk_load(sB + static_cast<size_t>(slot) * a.b_chunk_bytes, b_src(t, kc), a.b_chunk_bytes,
                       &b_full[slot]);
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               bph ^= 1;
             }
           }
-          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_wait(&a_empty[as], aph ^ 1, 3);
           mbar_arrive_expect_tx(&a_full[as], a.a_stage_bytes);
           uint8_t* dst = sA + static_cast<size_t>(as) * a.a_stage_bytes;
           if (a.stride == 1) {
@@ -202,26 +208,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     int acc = 0;
     uint32_t accph = 0;
     uint32_t bres_ph = 0;  // phase of the resident B slots (flips on every reload)
-    int mkey = -1;
+    // weight key of a tile = tile / per_key (member g, N tile nt); tracked with
+    // a compare per tile, a division only when the key changes
+    const bool multi_key = a.b_resident && (a.G > 1 || a.n_ntiles > 1);
+    const int per_key = a.Pm * a.mt_per_p;
+    int mkey = static_cast<int>(blockIdx.x) / per_key;
+    int kbound = (mkey + 1) * per_key;
     unsigned long long t_acc = 0, t_a = 0, t_issue = 0, t0 = 0;
     const bool prof = (a.dbg & 8) && a.prof;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-      if (a.b_resident) {
-        const TileIdx tt = decode_tile(a, tile);
-        const int key = tt.g * a.n_ntiles + tt.nt;
-        if (mkey >= 0 && key != mkey) bres_ph ^= 1;
-        mkey = key;
+      if (multi_key && tile >= kbound) {
+        bres_ph ^= 1;
+        mkey = tile / per_key;
+        kbound = (mkey + 1) * per_key;
       }
       if (prof) t0 = clock64();
-      mbar_wait(&acc_empty[acc], accph ^ 1);
+      mbar_wait(&acc_empty[acc], accph ^ 1, 10 + 1000 * static_cast<int>(bres_ph));
       if (prof) t_acc += clock64() - t0;
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bn);
       for (int kc = 0; kc < a.n_kchunks; ++kc) {
         const int slot = a.b_resident ? kc : bs;
         if (prof) t0 = clock64();
-        mbar_wait(&b_full[slot], a.b_resident ? bres_ph : bph);
-        mbar_wait(&a_full[as], aph);
+        mbar_wait(&b_full[slot], a.b_resident ? bres_ph : bph, 11 + 1000 * slot);
+        mbar_wait(&a_full[as], aph, 12 + 1000 * as);
         if (prof) {
           const unsigned long long t1 = clock64();
           t_a += t1 - t0;
@@ -308,6 +318,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       if (elect_one()) mma_commit(&acc_full[acc]);
       __syncwarp();
+      if (multi_key && tile + static_cast<int>(gridDim.x) >= kbound &&
+          tile + static_cast<int>(gridDim.x) < a.num_tiles) {  // the next tile needs other weights
+        if (elect_one()) mma_commit(&b_empty[0]);
+        __syncwarp();
+      }
       if (++acc == 2) {
         acc = 0;
         accph ^= 1;
@@ -364,11 +379,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
       }
-      const float* bias_t =
-          uniform_bias ? s_bias : a.bias + static_cast<size_t>(ti.g) * a.bias_stride + static_cast<size_t>(nt) * a.bn;
-      const float* fc_t = uniform_bias ? s_fc : a.fc_w + static_cast<size_t>(ti.g) * a.cout;
+      const float* bias_t = smem_bias ? s_bias + ti.g * a.bn
+                                      : a.bias + static_cast<size_t>(ti.g) * a.bias_stride +
+                                            static_cast<size_t>(nt) * a.bn;
+      const float* fc_t = smem_bias ? s_fc + ti.g * a.bn : a.fc_w + static_cast<size_t>(ti.g) * a.cout;
       if (eprof) et0 = clock64();
-      mbar_wait(&acc_full[acc], accph);
+      mbar_wait(&acc_full[acc], accph, 20 + 1000 * mt);
       if (eprof) {
         const unsigned long long t1 = clock64();
         e_wait += t1 - et0;
@@ -475,7 +491,9 @@ int conv_bn(int cout) {
   return round_up((c + nt - 1) / nt, 16);
 }
 
-constexpr uint32_t kFixedSmem = 1024 + 256 + 2048;  // barriers, holder/head scratch, bias/fc
+// barriers + holder/head scratch + per-member bias and fc (up to 1024 floats each)
+constexpr int kSmemBiasMax = 1024;
+constexpr uint32_t kFixedSmem = 1024 + 256 + 2 * kSmemBiasMax * 4;
 
 static int a_rows(int stride) { return stride == 1 ? kRowsS1 : kRowsS2; }
 
@@ -643,6 +661,7 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.wpack_stride = wpack_bytes(cin, cout);
   a.bias = bias;
   a.bias_stride = static_cast<int>(bias_len(cout));
+  a.sb_len = (a.n_ntiles == 1 && G * a.bn <= kSmemBiasMax) ? G * a.bn : 0;
   a.out = out;
   a.res = res;
   a.res_mode = res ? res_mode : 0;

@@ -173,6 +173,12 @@ struct ProfRec {
   std::vector<double> flops, bytes;
   void mark(cudaStream_t st, int k, double f, double b) {
     if (!ev) return;
+    static const bool dbg_sync = getenv("HB_DEBUG_SYNC") != nullptr;
+    if (dbg_sync) {
+      fprintf(stderr, "[hb] launch %zu kind %d ...", kind.size(), k);
+      const cudaError_t e = cudaStreamSynchronize(st);
+      fprintf(stderr, " %s\n", cudaGetErrorString(e));
+    }
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);

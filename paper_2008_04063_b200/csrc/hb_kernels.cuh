@@ -48,6 +48,7 @@ struct ConvArgs {
   size_t wpack_stride;             // bytes per member
   const float* bias;               // [G][n_ntiles*bn] (zero padded)
   int bias_stride;                 // floats per member
+  int sb_len;                      // floats of bias (and of fc) cached in smem: G*bn, 0 = read global
   __half* out;                     // output activation (layout out_split)
   const __half* res;               // shortcut source or null
   int res_mode;                    // 0 none, 1 identity (I layout), 2 maxpool(2) (S layout)

@@ -3,6 +3,7 @@
 // the reference (zooserve) is pure Python with no device path.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -57,8 +58,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Blocking wait with a watchdog: a wait that has not completed after ~2^22
+// suspended try_waits (several seconds) is a pipeline bug, not slowness —
+// report which barrier/tag and trap instead of hanging the GPU.
+// (Build with -DHB_WATCHDOG_VERBOSE to print the stuck barrier's tag; the
+// default trap is a bare instruction so hot loops keep no call frame.)
+#ifdef HB_WATCHDOG_VERBOSE
+static __device__ __noinline__ void mbar_stuck(int tag, uint32_t parity) {
+  printf("[hb watchdog] block %d thread %d tag %d parity %u stuck\n", blockIdx.x, threadIdx.x, tag, parity);
+  __trap();
+}
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1u << 22)) {
+#ifdef HB_WATCHDOG_VERBOSE
+      mbar_stuck(tag, parity);
+#else
+      (void)tag;
+      asm volatile("trap;");
+#endif
+    }
   }
 }
 

@@ -101,7 +101,7 @@ def test_serving_loop_realtime():
     assert [t.query_id for t in tr] == list(range(P * n_ticks))
     pc = tick_latency_percentiles(tr, P)
     assert pc["p99"] < 0.2
-    ml, _, _ = cpu_path.cpu_tick(zoo, sel, streams, 7500 + hop * n_ticks)
+    ml, _, _ = cpu_path.cpu_tick(zoo, sel, streams, 7500 + hop * (n_ticks - 1))
     last = tr[-P:]
     got = np.array([[t.model_scores[zoo.profiles[i].id] for i in sel.indices()] for t in last])
     assert np.abs(got - ml).max() <= 2e-2
