@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-patients", type=int, default=8, help="CPU baseline sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks / cpu)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the 1024-bed and profiler-sweep side measurements")
     return ap.parse_args()
 
 
@@ -84,7 +85,7 @@ class Clocks:
     def __init__(self, index: int):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", str(index)], stdout=subprocess.PIPE,
+                                       "-lms", "20", "-i", str(index)], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
@@ -152,6 +153,66 @@ def cpu_baseline(zoo, sel, n_patients, seed=0):
     return {"value": n_patients / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
             "sample": f"{n_patients} patient-windows x 4 members (one c2 tick subset), PyTorch fp32 CPU oracle, "
                       f"{dt:.2f} s"}
+
+
+def tick_at(zoo, sel, P, hop, device, K=30, warm=5):
+    """North-star side measurement: the same ensemble at P beds (graph tick, device time, L2 flushed)."""
+    import torch
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    eng = EnsembleEngine(zoo, sel, P, hop=hop, device=device)
+    eng.ingest((np.random.default_rng(1).standard_normal((P, 3, 7500)) * 0.3).astype(np.float32))
+    blk = torch.randn(P, 3, hop, device="cuda") * 0.3
+    st = torch.cuda.Stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ms = []
+    with torch.cuda.stream(st):
+        for i in range(warm + K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            eng.stage_device(blk.data_ptr(), st.cuda_stream)
+            eng.tick_device(st.cuda_stream)
+            b.record(st)
+            if i >= warm:
+                ms.append((a, b))
+    torch.cuda.synchronize()
+    t = [a.elapsed_time(b) for a, b in ms]
+    flops, _ = eng.tick_work()
+    eng.close()
+    return {"patients": P, "tick_ms_p50": pct(t, 50), "tick_ms_p99": pct(t, 99),
+            "patient_windows_per_s": P / (float(np.mean(t)) / 1e3),
+            "tflops": flops / (float(np.mean(t)) / 1e3) / 1e12, "ticks": K}
+
+
+def sweep_bench(device):
+    """Config c4: exhaustive profiler sweep over N=20000 recorded windows (synthetic cohort),
+    n=10 (1023 candidates) and n=16 (65535), K6 on the device; CPU oracle on a bounded sample."""
+    from oracle import auc as oauc
+    from paper_2008_04063_b200 import cohort as hc
+    from paper_2008_04063_b200 import composer
+    from paper_2008_04063_b200.zoo import generate_zoo
+    out = {}
+    for n, grid in ((10, ([8, 16, 32, 64, 128], [2, 4])), (16, ([8, 16, 32, 64], [2, 4, 8, 16]))):
+        z = generate_zoo(1, grid[0], grid[1], seed=3)
+        coh = hc.synthesize_cohort(z, 10000, 10000, 0.5, 0)
+        dev = coh.device(device)
+        dev.auc_range(1, 64)                       # warm
+        t0 = time.perf_counter()
+        aucs = composer.sweep_aucs(coh, device)
+        dt = time.perf_counter() - t0
+        best = int(np.argmax(aucs)) + 1
+        S = (1 << n) - 1
+        out[f"n{n}"] = {"candidates": S, "N": 20000, "seconds": dt, "candidates_per_s": S / dt,
+                        "best_auc_selector": format(best, f"0{n}b")[::-1], "best_auc": float(aucs[best - 1])}
+    # CPU oracle (same algorithm, numpy, 1 core) on a bounded sample of the n=10 sweep
+    z = generate_zoo(1, [8, 16, 32, 64, 128], [2, 4], seed=3)
+    coh = hc.synthesize_cohort(z, 10000, 10000, 0.5, 0)
+    vals = np.arange(1, 65)
+    t0 = time.perf_counter()
+    oauc.sweep(coh.labels, coh.scores, vals)
+    dt = time.perf_counter() - t0
+    out["cpu_oracle"] = {"candidates_per_s": len(vals) / dt, "cores": 1, "sample": "64 candidates of n=10, N=20000"}
+    return out
 
 
 def run_reference(args):
@@ -246,7 +307,6 @@ def run_b200(args):
             eng.tick_device(stream.cuda_stream)
             evs[i][1].record(stream)
     torch.cuda.synchronize()
-    ck = clocks.stop() if clocks else None
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = allmax(float(sum(step_ms)))
     barrier()
@@ -281,6 +341,7 @@ def run_b200(args):
     for i in range(K):
         eng.tick(hin[Wu + i], out=out)
     e2e_s = allmax(time.perf_counter() - t0)
+    ck = clocks.stop() if clocks else None
     e2e_value = world * P * K / e2e_s
     h2d = P * 3 * hop * 4
     d2h = P * M * 4 + 2 * P * 4
@@ -288,6 +349,11 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu = cpu_baseline(zoo, sel, args.cpu_patients)
+    extras = {}
+    if rank == 0 and world == 1 and not args.profile_only and not args.no_extras:
+        eng.close()
+        extras["beds_1024"] = tick_at(zoo, sel, 1024, hop, local)
+        extras["profiler_sweep"] = sweep_bench(local)
 
     cfg = workload(args)
     cfg["tick_latency_ms"] = {"p50": p50, "p95": p95, "p99": p99, "slo": SLO_MS}
@@ -296,6 +362,7 @@ def run_b200(args):
         "conv_tcgen05": conv_ms, "aggregate": float(ms[kinds == 3].sum() + ms[kinds == 4].sum()),
         "total": tick_ms_eager}
     cfg["tick_flops"] = float(flops.sum())
+    cfg.update(extras)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wu,
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -312,7 +379,8 @@ def run_b200(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    eng.close()
+    if not extras:
+        eng.close()
     if world > 1:
         dist.destroy_process_group()
 
