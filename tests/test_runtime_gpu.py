@@ -105,3 +105,31 @@ def test_serving_loop_realtime():
     last = tr[-P:]
     got = np.array([[t.model_scores[zoo.profiles[i].id] for i in sel.indices()] for t in last])
     assert np.abs(got - ml).max() <= 2e-2
+
+
+def test_binary_ingest_server_ticks_match_direct_engine():
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    from paper_2008_04063_b200.serving import BinaryIngestServer, send_frames
+    import time
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [10, 13])
+    P, hop = 4, 250
+    streams = synth.ecg_block(8, P, 3, 0, 7500 + 3 * hop)
+    frames = [streams[:, :, 7500 + k * hop - hop:7500 + k * hop] for k in range(4)]
+    got = []
+    with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+        eng.ingest(streams[:, :, :7500 - hop])
+        srv = BinaryIngestServer(eng, on_result=lambda k, r: got.append((k, r.ens_prob.copy())))
+        srv.start()
+        try:
+            send_frames(srv.address, frames)
+            t0 = time.time()
+            while len(got) < 4 and time.time() - t0 < 30:
+                time.sleep(0.01)
+        finally:
+            srv.stop()
+    assert [k for k, _ in got] == [0, 1, 2, 3] and srv.errors == []
+    with EnsembleEngine(zoo, sel, P, hop=hop) as ref:
+        ref.ingest(streams[:, :, :7500 - hop])
+        for k, f in enumerate(frames):
+            assert np.array_equal(ref.tick(f).ens_prob, got[k][1])
