@@ -353,6 +353,7 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.profile_only and not args.no_extras:
         eng.close()
         extras["beds_1024"] = tick_at(zoo, sel, 1024, hop, local)
+        extras["c3_full_zoo_100_beds"] = tick_at(zoo, Selector.ones(60), 100, hop, local, K=10, warm=2)
         extras["profiler_sweep"] = sweep_bench(local)
 
     cfg = workload(args)

@@ -382,7 +382,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const float* bias_t = smem_bias ? s_bias + ti.g * a.bn
                                       : a.bias + static_cast<size_t>(ti.g) * a.bias_stride +
                                             static_cast<size_t>(nt) * a.bn;
-      const float* fc_t = smem_bias ? s_fc + ti.g * a.bn : a.fc_w + static_cast<size_t>(ti.g) * a.cout;
+      const float* fc_t = smem_bias ? s_fc + ti.g * a.bn
+                                    : a.fc_w + static_cast<size_t>(ti.g) * a.cout + static_cast<size_t>(nt) * a.bn;
       if (eprof) et0 = clock64();
       mbar_wait(&acc_full[acc], accph, 20 + 1000 * mt);
       if (eprof) {
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         named_bar_sync(1 + eg, 128);
         if (wq == 0 && lane == 0) {
           const float sum = ((sh[0] + sh[1]) + sh[2]) + sh[3];
-          a.head_out[static_cast<size_t>(p) * a.mt_per_p + mt] = sum;  // n_ntiles == 1 enforced for heads
+          a.head_out[(static_cast<size_t>(p) * a.n_ntiles + nt) * a.mt_per_p + mt] = sum;
         }
         named_bar_sync(1 + eg, 128);
       }
@@ -618,7 +619,6 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.cout = cout;
   a.bn = conv_bn(cout);
   a.n_ntiles = (round_up(cout, 16) + a.bn - 1) / a.bn;
-  if (fc_w && a.n_ntiles != 1) return "conv: fused head needs cout <= 256";
   a.lin = lin;
   a.lout = lout;
   a.out_split = out_split;

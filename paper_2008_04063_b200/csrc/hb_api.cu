@@ -318,7 +318,10 @@ int build_selection(hb_ctx* c) {
       g.bias.push_back(b);
     }
     CK(c, cudaMalloc(&g.fc_w, sizeof(float) * c_last * G));
-    g.head_mt = (g.layers.back().lout + kBM - 1) / kBM;
+    {  // head partials per (patient, N tile, M tile) of the last layer
+      const int cl = g.layers.back().cout, bn = conv_bn(cl);
+      g.head_mt = ((round_up(cl, 16) + bn - 1) / bn) * ((g.layers.back().lout + kBM - 1) / kBM);
+    }
     CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P * g.head_mt));
     for (int k = 0; k < G; ++k) {
       const Member& m = c->members[c->selected[g.mi[k]]];

@@ -54,7 +54,7 @@ struct ConvArgs {
   int res_mode;                    // 0 none, 1 identity (I layout), 2 maxpool(2) (S layout)
   int res_c, res_rows;             // shortcut channels; plane rows (I: lp, S: lh)
   int relu;
-  const float* fc_w;               // head: [G][cout] -> head_out[G*Pm][mt_per_p] (null = no head)
+  const float* fc_w;               // head: [G][cout] -> head_out[G*Pm][n_ntiles][mt_per_p] (null = no head)
   float* head_out;
   int dbg;                         // experiments only (HB_DEBUG env)
   unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]

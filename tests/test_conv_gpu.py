@@ -56,7 +56,9 @@ def run_conv(x, w, b, stride, res=None, res_mode=0, fc_w=None, out_split=0):
     rin = None
     if res is not None:
         rin = to_split(res.to(dev)) if res_mode == 2 else to_ng8(res.to(dev))
-    head = torch.zeros(P, (lout + 127) // 128, dtype=torch.float32, device=dev) if fc_w is not None else None
+    c16 = (max(cout, 16) + 15) // 16 * 16
+    n_nt = 1 if c16 <= 256 else -(-c16 // 256)              # N tiles (conv_bn in conv_tc.cu)
+    head = torch.zeros(P, n_nt * ((lout + 127) // 128), dtype=torch.float32, device=dev) if fc_w is not None else None
     wn = np.ascontiguousarray(w.numpy(), np.float32)
     bn = np.ascontiguousarray(b.numpy(), np.float32)
     fcn = np.ascontiguousarray(fc_w.numpy(), np.float32) if fc_w is not None else None
@@ -148,9 +150,11 @@ def test_layout_padding_edges(L):
         assert torch.allclose(from_ng8(out2, c, l2).float().cpu(), ref_conv(x2, w, b, 2), rtol=2e-3, atol=2e-3)
 
 
-def test_conv_fused_head():
+@pytest.mark.parametrize("c", [64, 512])
+def test_conv_fused_head(c):
+    """Last conv + mean-pool + FC in the epilogue; 512 channels = two N tiles of partials."""
     g = torch.Generator().manual_seed(5)
-    P, c, lin = 3, 64, 469
+    P, lin = 3, 469
     x = torch.relu(_rand((P, c, lin), g))
     blk = torch.relu(_rand((P, c, 938), g))
     w = _rand((c, c, 16), g, (2.0 / (c * 16)) ** 0.5)

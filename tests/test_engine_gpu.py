@@ -111,3 +111,16 @@ def test_empty_selector_rejected():
     from paper_2008_04063_b200.errors import EmptyEnsembleError
     with pytest.raises(EmptyEnsembleError):
         EnsembleEngine(holmes_zoo(), Selector.zeros(60), 2)
+
+
+def test_full_zoo_c3_matches_oracle():
+    """Config c3's ensemble: all 60 members (every width 8..128 x depth 2..16 x lead),
+    incl. streamed weights and multi-N-tile layers (w128-d16 reaches 1024 channels)."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.ones(60)
+    P, W = 2, 7500
+    streams = _streams(P, W, seed=11)
+    with EnsembleEngine(zoo, sel, P, hop=W) as eng:
+        res = eng.tick(streams)
+    _compare(res, *_oracle_tick(zoo, sel, streams, W))
