@@ -16,4 +16,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:inge
   -o gpurun_out/prof_window -f python tools/prof1.py 10,13,30,50 > gpurun_out/ncu_window.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_auc -c 1 \
   -o gpurun_out/prof_sweep -f python tools/sweep1.py > gpurun_out/ncu_sweep.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 20 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/bench_torchrun.json 2> gpurun_out/bench_torchrun.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; head -c 600 gpurun_out/bench.json; echo; cat gpurun_out/conv_traffic.json | head -8
