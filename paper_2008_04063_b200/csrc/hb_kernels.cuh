@@ -102,12 +102,13 @@ cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st);
 // one-time kernel attribute setup (opt-in shared memory); call before capture.
 cudaError_t init_conv_kernel();
 cudaError_t init_stream_kernels();
+cudaError_t init_stem_kernel();
 inline cudaError_t init_kernels() {
   cudaError_t e = init_conv_kernel();
   return e != cudaSuccess ? e : init_stream_kernels();
 }
 
-// stem conv (C_in = 1) + bias + ReLU on CUDA cores for G members of one
+// stem conv (C_in = 1) + bias + ReLU on tcgen05 (one K=16 MMA per tile) for G members of one
 // group: member g reads xn + x_off[g] ([Pm][L] fp16), weights w[g][cout][16],
 // b[g][cout]; writes rows [g*Pm, (g+1)*Pm) of the NG8 output.
 struct StemMember {

@@ -1,5 +1,5 @@
-// K1/K2 (ring append, window gather, z-normalisation), K3 (stem conv on CUDA
-// cores) and K5 (head + ensemble aggregation).  All memory-bound or tiny.
+// K1/K2 (ring append, window gather, z-normalisation) and K5 (head + ensemble
+// aggregation).  Both memory-bound or tiny.  (K3, the stem, is stem_tc.cu.)
 //
 // Reference counterparts (behaviour, not code):
 //   K1/K2 replace `Aggregator.add` buffering + `WindowBatch` materialisation
@@ -114,101 +114,13 @@ cudaError_t launch_ingest_window(const float* staged, float* ring, const long lo
 }
 
 cudaError_t init_stream_kernels() {
-  return cudaFuncSetAttribute(ingest_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const cudaError_t e = cudaFuncSetAttribute(ingest_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+  return e != cudaSuccess ? e : init_stem_kernel();
 }
 
 cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st) {
   return launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, wpos, n);
-}
-
-// ------------------------------------------------------------------ K3 stem
-// out[p][g][l][8] = ReLU(b + sum_t w[c][t] * x[p][l + t - pad]),  rows [L, Lp) = 0.
-// One CTA = 1024 positions of one (member, patient) row; each thread owns 4
-// consecutive positions (19 samples in registers) and walks the channels
-// 8 at a time, weights broadcast from shared memory as float4.  The output
-// rows of one 8-channel plane are written as 4 x 16 B per thread (a warp
-// writes 2 KB contiguous).
-constexpr int kStemThreads = 256;
-constexpr int kStemPos = 4;
-constexpr int kStemTile = kStemThreads * kStemPos;
-struct StemArgs {
-  StemMember m[kMaxGroup];
-  int Pm, x_stride, L, lp_out, cout, pad;
-  __half* out;
-};
-
-__global__ void __launch_bounds__(kStemThreads) stem_kernel(const __grid_constant__ StemArgs a) {
-  __shared__ float sx[kStemTile + kTaps];
-  __shared__ __align__(16) float sw[128 * kTaps];
-  __shared__ float sb[128];
-  const int row = blockIdx.y;            // g * Pm + p
-  const int g = row / a.Pm, p = row - g * a.Pm;
-  const int l0 = blockIdx.x * kStemTile;
-  const StemMember& mb = a.m[g];
-  for (int i = threadIdx.x; i < a.cout * kTaps; i += kStemThreads) sw[i] = mb.w[i];
-  for (int i = threadIdx.x; i < a.cout; i += kStemThreads) sb[i] = mb.b[i];
-  pdl_wait();   // x is the window kernel's output
-  pdl_trigger();
-  const __half* x = mb.x + static_cast<size_t>(p) * a.x_stride;
-  for (int i = threadIdx.x; i < kStemTile + kTaps; i += kStemThreads) {
-    const int pos = l0 + i - a.pad;
-    sx[i] = (pos >= 0 && pos < a.L) ? __half2float(x[pos]) : 0.f;
-  }
-  __syncthreads();
-  const int lt = threadIdx.x * kStemPos;
-  const int l = l0 + lt;
-  if (l >= a.lp_out) return;
-  float xv[kStemPos + kTaps - 1];
-#pragma unroll
-  for (int t = 0; t < kStemPos + kTaps - 1; ++t) xv[t] = sx[lt + t];
-  const int G8 = a.cout / 8;
-  __half* orow = a.out + static_cast<size_t>(row) * G8 * a.lp_out * 8;
-  for (int g8 = 0; g8 < G8; ++g8) {
-    float acc[kStemPos][8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float bj = sb[g8 * 8 + j];
-#pragma unroll
-      for (int q = 0; q < kStemPos; ++q) acc[q][j] = bj;
-      const float4* wj = reinterpret_cast<const float4*>(sw + (g8 * 8 + j) * kTaps);
-#pragma unroll
-      for (int t4 = 0; t4 < kTaps / 4; ++t4) {
-        const float4 w4 = wj[t4];
-        const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int q = 0; q < kStemPos; ++q) acc[q][j] = fmaf(wv[u], xv[q + 4 * t4 + u], acc[q][j]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kStemPos; ++q) {
-      if (l + q >= a.lp_out) break;
-      const bool valid = l + q < a.L;
-      uint4 pk;
-      __half2* o2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-      for (int j = 0; j < 8; j += 2)
-        o2[j / 2] = valid ? __floats2half2_rn(fmaxf(acc[q][j], 0.f), fmaxf(acc[q][j + 1], 0.f))
-                          : __floats2half2_rn(0.f, 0.f);
-      *reinterpret_cast<uint4*>(orow + (static_cast<size_t>(g8) * a.lp_out + l + q) * 8) = pk;
-    }
-  }
-}
-
-cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int lp_out, int cout, int pad,
-                        __half* out, cudaStream_t st) {
-  if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup) return cudaErrorInvalidValue;
-  StemArgs a;
-  for (int g = 0; g < G; ++g) a.m[g] = members[g];
-  a.Pm = Pm;
-  a.x_stride = x_stride;
-  a.L = L;
-  a.lp_out = lp_out;
-  a.cout = cout;
-  a.pad = pad;
-  a.out = out;
-  return launch_pdl(stem_kernel, dim3((lp_out + kStemTile - 1) / kStemTile, G * Pm), dim3(kStemThreads), 0, st, a);
 }
 
 // ------------------------------------------------------------------ K5 aggregate
