@@ -155,6 +155,24 @@ def cpu_baseline(zoo, sel, n_patients, seed=0):
                       f"{dt:.2f} s"}
 
 
+def tick_roofline(zoo, sel, P, peak_tf, peak_gbs):
+    """Tick roofline time: sum over every layer of max(FLOPs / tensor peak, algorithmic
+    bytes / HBM peak) — input + output (+ shortcut) activations in fp16, per window."""
+    from paper_2008_04063_b200 import arch
+    t = f_tot = b_tot = 0.0
+    for i in sel.indices():
+        pr = zoo.profiles[i]
+        for L in arch.member_layers(pr.width, pr.depth):
+            f = L.flops * P
+            b = (L.cin * L.lin + (0 if L.head else L.cout * L.lout) +
+                 (L.res_c * L.lin if L.res != "none" else 0)) * 2 * P
+            t += max(f / (peak_tf * 1e12), b / (peak_gbs * 1e9))
+            f_tot += f
+            b_tot += b
+    return {"ms": t * 1e3, "flops": f_tot, "bytes": b_tot,
+            "def": "sum_layers max(FLOPs/sustained tensor peak, (in+out+shortcut) fp16 bytes/HBM peak)"}
+
+
 def tick_at(zoo, sel, P, hop, device, K=30, warm=5):
     """North-star side measurement: the same ensemble at P beds (graph tick, device time, L2 flushed)."""
     import torch
@@ -363,6 +381,9 @@ def run_b200(args):
         "conv_tcgen05": conv_ms, "aggregate": float(ms[kinds == 3].sum() + ms[kinds == 4].sum()),
         "total": tick_ms_eager}
     cfg["tick_flops"] = float(flops.sum())
+    roof = tick_roofline(zoo, sel, P, peak_tf, peak_hbm)
+    roof["frac_of_measured_p50"] = roof["ms"] / p50
+    cfg["tick_roofline"] = roof
     cfg.update(extras)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wu,
