@@ -157,6 +157,17 @@ int hb_cohort_ensemble(hb_cohort* c, const uint8_t* bits, double* ens_out, doubl
 int hb_sweep_auc(int device, const double* scores, const int8_t* labels, int N, int n, const uint32_t* selectors,
                  int S, double* auc_out);
 
+/* ---------------------------------------------------------------- K7 curves
+ * Arrival-curve construction for the latency profiler's queueing bound
+ * (replaces the quadratic loops of build_arrival_curve, latency.py:198-239).
+ * Host buffers in and out; bit-identical to the reference's numpy results.
+ *   hb_arrival_widths: widths[c-1] = min_i ts[i+c-1] - ts[i], c = 1..m (ts sorted)
+ *   hb_binned_best:    best[k-1]  = max_j csum[j+k] - csum[j], k = 1..n_bins
+ *                      (csum has n_bins + 1 entries) */
+int hb_arrival_widths(const double* ts, int m, double* widths_out);
+int hb_binned_best(const double* csum, int n_bins, double* best_out);
+const char* hb_curve_last_error(void);
+
 /* Kernel-level entry points used by the parity tests (device pointers).
  * Activation layouts (fp16, 8-channel groups g, see hb_kernels.cuh):
  *   I: [P][C/8][roundup(L,8)][8];  S: [P][C/8][2][roundup(ceil(L/2),8)][8] (even/odd positions).

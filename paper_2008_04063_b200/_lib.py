@@ -66,6 +66,9 @@ _SIGS = {
     "hb_cohort_auc": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_double)]),
     "hb_cohort_auc_range": (C.c_int, [_P, C.c_ulonglong, C.c_longlong, C.POINTER(C.c_double)]),
     "hb_cohort_ensemble": (C.c_int, [_P, C.POINTER(C.c_uint8), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "hb_arrival_widths": (C.c_int, [C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double)]),
+    "hb_binned_best": (C.c_int, [C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_double)]),
+    "hb_curve_last_error": (C.c_char_p, []),
     "hb_op_conv1d": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
                                C.c_int, _P, C.c_int, _F, _P, _P]),
     "hb_bench_conv": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
@@ -104,7 +107,8 @@ def check(rc: int, ctx=None, getter: str = "hb_last_error") -> None:
     """Raise the reference's exception class for a non-zero status (errors.py)."""
     if rc == HB_OK:
         return
-    msg = getattr(lib(), getter)(ctx)
+    fn = getattr(lib(), getter)
+    msg = fn() if getter == "hb_curve_last_error" else fn(ctx)
     text = msg.decode() if msg else f"status {rc}"
     raise _EXC.get(rc, RuntimeError)(text)
 

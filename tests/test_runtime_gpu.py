@@ -133,3 +133,15 @@ def test_binary_ingest_server_ticks_match_direct_engine():
         ref.ingest(streams[:, :, :7500 - hop])
         for k, f in enumerate(frames):
             assert np.array_equal(ref.tick(f).ens_prob, got[k][1])
+
+
+@pytest.mark.parametrize("patients,jitter", [(16, 2.5e-4), (200, 2.5e-4), (8192, 2.5e-4), (3, 0.0)])
+def test_device_arrival_curve_bit_identical(patients, jitter):
+    """K7 vs the host formulation (= the reference's numpy loops): exact path
+    (<= 8000 events) and binned path (8192 beds -> 16384 events, ~30 000 bins)."""
+    sysc = latency.SystemConfig(patients=patients)
+    tr = latency.profiling_trace(sysc, seed=1, jitter_s=jitter)
+    a = latency.build_arrival_curve(tr, backend="host")
+    b = latency.build_arrival_curve(tr, backend="device")
+    assert np.array_equal(a.dts, b.dts) and np.array_equal(a.counts, b.counts)
+    assert a.n_events == b.n_events and a.span_s == b.span_s
