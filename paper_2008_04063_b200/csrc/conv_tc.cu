@@ -465,7 +465,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         named_bar_sync(1 + eg, 128);
         if (wq == 0 && lane == 0) {
           const float sum = ((sh[0] + sh[1]) + sh[2]) + sh[3];
-          a.head_out[(static_cast<size_t>(p) * a.n_ntiles + nt) * a.mt_per_p + mt] = sum;
+          a.head_out[static_cast<size_t>(ti.g) * a.head_g_stride +
+                     (static_cast<size_t>(p - ti.g * a.Pm) * a.n_ntiles + nt) * a.mt_per_p + mt] = sum;
         }
         named_bar_sync(1 + eg, 128);
       }
@@ -604,7 +605,7 @@ bool pdl_enabled() {
 const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                       const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
                       const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
-                      float* head_out, int num_sms) {
+                      float* head_out, int num_sms, size_t head_g_stride) {
   std::memset(plan, 0, sizeof(*plan));
   if (G < 1 || G > kMaxGroup || Pm < 1) return "conv: bad group shape";
   const int P = G * Pm;
@@ -671,6 +672,7 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.relu = 1;
   a.fc_w = fc_w;
   a.head_out = head_out;
+  a.head_g_stride = head_g_stride ? head_g_stride : static_cast<size_t>(Pm) * a.n_ntiles * a.mt_per_p;
   a.dbg = dbg;
   plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + kFixedSmem;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;

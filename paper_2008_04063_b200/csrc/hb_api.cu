@@ -52,14 +52,14 @@ struct Group {
   int width = 0, depth = 0, lead_any = 0, lane = 0;
   std::vector<int> mi;                 // positions in hb_ctx::selected (zoo order)
   std::vector<LayerSpec> layers;
-  std::vector<StemMember> stem;        // per member: its lead's normalised windows, stem weights
+  std::vector<std::vector<StemMember>> stem;  // [chunk][member]: its lead's windows (chunk rows), stem weights
   std::vector<uint8_t*> wpack;         // per conv layer: [G][member image]
   std::vector<float*> bias;            // per conv layer: [G][bias_len]
   float* fc_w = nullptr;               // [G][c_last]
   float* head_partial = nullptr;       // [G*P][mt]
   int head_mt = 0;
   double flops = 0;
-  size_t plan0 = 0;                    // first plan index
+  std::vector<size_t> plan0;           // first plan index, per patient chunk
 };
 
 struct Member {
@@ -81,6 +81,10 @@ struct hb_ctx {
   int device = 0, P = 0, leads = 0, fs = 0, W = 0, hop = 0, R = 0, keep = 0, num_sms = 148;
   int max_lanes = 4;  // concurrent member branches in the tick graph (HB_LANES overrides)
   int group_off = 0;  // HB_NO_GROUP=1: one launch per member and layer (A/B experiments)
+  // patient micro-batching: member chains run over chunks of Pc beds so the
+  // activation buffers stay within act_budget (the rings / windows hold all P)
+  int Pc = 0, n_chunks = 1, P_pad = 0;
+  double act_budget = 64e9;
   cudaStream_t own = nullptr;
   float* ring = nullptr;
   float* staged = nullptr;   // [P][leads][hop]
@@ -141,6 +145,8 @@ void free_selection(hb_ctx* c) {
     cudaFree(g.head_partial);
   }
   c->groups.clear();
+  cudaFree(c->xn);
+  c->xn = nullptr;
   for (auto s2 : c->side) cudaStreamDestroy(s2);
   c->side.clear();
   for (auto e : c->ev) cudaEventDestroy(e);
@@ -194,7 +200,7 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   ProfRec none;
   if (!pr) pr = &none;
   const double P = c->P;
-  CK(c, launch_ingest_window(c->staged, c->ring, c->wpos, c->P, c->leads, c->hop, c->R, c->W, c->xn,
+  CK(c, launch_ingest_window(c->staged, c->ring, c->wpos, c->P, c->leads, c->hop, c->R, c->W, c->xn, c->P_pad,
                              c->keep ? c->raw : nullptr, c->stats, st));
   pr->mark(st, K_INGEST, 0.0, P * c->leads * (c->hop * 8.0 + c->W * 6.0));
   // Members fork into `lanes` branches after the window kernel and join before
@@ -211,19 +217,22 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
       CK(c, cudaStreamWaitEvent(ms, c->ev[0], 0));
       lane_started[ln] = true;
     }
-    __half* const* act = &c->act[3 * ln];
     const int G = static_cast<int>(g.mi.size());
-    const double rows = P * G;
+    const double rows = static_cast<double>(c->Pc) * G;
     const LayerSpec& s0 = g.layers[0];
-    CK(c, launch_stem(g.stem.data(), G, c->W, c->P, c->W, round_up(s0.lout, 8), s0.cout, s0.pad, act[0], ms));
-    pr->mark(ms, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
-    size_t pi = g.plan0;
-    for (size_t li = 1; li < g.layers.size(); ++li) {
-      const LayerSpec& L = g.layers[li];
-      CK(c, launch_conv(c->plans[pi++], ms));
-      pr->mark(ms, K_CONV, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
-               rows * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
-                             (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
+    for (int ch = 0; ch < c->n_chunks; ++ch) {
+      CK(c, launch_stem(g.stem[ch].data(), G, c->W, c->Pc, c->W, round_up(s0.lout, 8), s0.cout, s0.pad,
+                        c->act[3 * ln], ms));
+      pr->mark(ms, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+      size_t pi = g.plan0[ch];
+      for (size_t li = 1; li < g.layers.size(); ++li) {
+        const LayerSpec& L = g.layers[li];
+        CK(c, launch_conv(c->plans[pi++], ms));
+        pr->mark(ms, K_CONV, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
+                 rows * 2.0 * (static_cast<double>(L.cin) * L.lin +
+                               (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
+                               (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));
+      }
     }
   }
   if (fork) {
@@ -276,12 +285,29 @@ int build_selection(hb_ctx* c) {
       load[ln] += c->groups[i].flops;
     }
   }
-  // activation buffers per lane, sized for the largest layer of its groups
+  // activation buffers per lane, sized for the largest layer of its groups at
+  // Pc beds; Pc halves until 3 rotating buffers per lane fit the budget
   std::vector<size_t> need(c->lanes, 0);
-  for (auto& g : c->groups)
-    for (auto& L : g.layers)
-      need[g.lane] = std::max(need[g.lane], static_cast<size_t>(c->P) * g.mi.size() * L.cout *
-                                                act_rows(L.lout, 1) * sizeof(__half));
+  auto size_for = [&](int pc) {
+    std::fill(need.begin(), need.end(), 0);
+    for (auto& g : c->groups)
+      for (auto& L : g.layers)
+        need[g.lane] = std::max(need[g.lane], static_cast<size_t>(pc) * g.mi.size() * L.cout *
+                                                  act_rows(L.lout, 1) * sizeof(__half));
+    double tot = 0;
+    for (size_t v : need) tot += 3.0 * v;
+    return tot;
+  };
+  c->Pc = c->P;
+  while (c->Pc > 1 && size_for(c->Pc) > c->act_budget) c->Pc = (c->Pc + 1) / 2;
+  size_for(c->Pc);
+  c->n_chunks = (c->P + c->Pc - 1) / c->Pc;
+  c->P_pad = c->n_chunks * c->Pc;
+  {  // normalised windows [leads][P_pad][W]; rows past P stay zero (padding beds of the last chunk)
+    const size_t xb = static_cast<size_t>(c->leads) * c->P_pad * c->W * sizeof(__half);
+    CK(c, cudaMalloc(&c->xn, xb));
+    CK(c, cudaMemset(c->xn, 0, xb));
+  }
   c->act.assign(3 * c->lanes, nullptr);
   for (int ln = 0; ln < c->lanes; ++ln)
     for (int k = 0; k < 3; ++k) {
@@ -322,16 +348,21 @@ int build_selection(hb_ctx* c) {
       const int cl = g.layers.back().cout, bn = conv_bn(cl);
       g.head_mt = ((round_up(cl, 16) + bn - 1) / bn) * ((g.layers.back().lout + kBM - 1) / kBM);
     }
-    CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P * g.head_mt));
+    CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P_pad * g.head_mt));
+    g.stem.assign(c->n_chunks, {});
     for (int k = 0; k < G; ++k) {
       const Member& m = c->members[c->selected[g.mi[k]]];
       CK(c, cudaMemcpy(g.fc_w + c_last * k, m.fc_w, sizeof(float) * c_last, cudaMemcpyDeviceToDevice));
-      g.stem.push_back({c->xn + static_cast<size_t>(m.lead) * c->P * c->W, m.stem_w, m.stem_b});
-      heads[g.mi[k]] = {g.head_partial + static_cast<size_t>(k) * c->P * g.head_mt, g.head_mt,
+      for (int ch = 0; ch < c->n_chunks; ++ch)
+        g.stem[ch].push_back(
+            {c->xn + (static_cast<size_t>(m.lead) * c->P_pad + static_cast<size_t>(ch) * c->Pc) * c->W, m.stem_w,
+             m.stem_b});
+      heads[g.mi[k]] = {g.head_partial + static_cast<size_t>(k) * c->P_pad * g.head_mt, g.head_mt,
                         1.f / static_cast<float>(g.layers.back().lout), m.fc_b};
     }
     __half* const* act = &c->act[3 * g.lane];
-    g.plan0 = c->plans.size();
+    for (int ch = 0; ch < c->n_chunks; ++ch) {
+    g.plan0.push_back(c->plans.size());
     int cur = 0;
     const int nblocks = static_cast<int>(g.layers.size() - 1) / 2;
     for (size_t li = 1; li < g.layers.size(); ++li) {
@@ -351,13 +382,16 @@ int build_selection(hb_ctx* c) {
         out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
       }
       ConvPlan plan;
-      const char* e = plan_conv(&plan, G, c->P, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+      // head partials of chunk ch: rows [ch*Pc, (ch+1)*Pc) of every member's [P_pad][head_mt] block
+      float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
+      const char* e = plan_conv(&plan, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
                                 L.head ? nullptr : act[dst], out_split, g.wpack[li - 1], g.bias[li - 1], res,
-                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr,
-                                L.head ? g.head_partial : nullptr, c->num_sms);
+                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr, head_base,
+                                c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
       if (e) return fail(c, HB_E_INVALID, e);
       c->plans.push_back(plan);
       if (!conv1) cur = dst;
+    }
     }
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
@@ -412,6 +446,7 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   c->keep = cfg->keep_windows;
   if (getenv("HB_LANES")) c->max_lanes = std::max(1, atoi(getenv("HB_LANES")));
   if (getenv("HB_NO_GROUP")) c->group_off = atoi(getenv("HB_NO_GROUP"));
+  if (getenv("HB_ACT_BUDGET_GB")) c->act_budget = atof(getenv("HB_ACT_BUDGET_GB")) * 1e9;
   if (c->R < c->W) {
     delete c;
     return fail(nullptr, HB_E_CONFIG, "ring_len must be >= window_len");
@@ -425,7 +460,6 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
             cudaMalloc(&c->prefill, S * c->R * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&c->wpos, sizeof(long long)) == cudaSuccess &&
             cudaMemset(c->wpos, 0, sizeof(long long)) == cudaSuccess &&
-            cudaMalloc(&c->xn, S * c->W * sizeof(__half)) == cudaSuccess &&
             cudaMalloc(&c->stats, S * 2 * sizeof(float)) == cudaSuccess &&
             cudaEventCreate(&c->t0) == cudaSuccess && cudaEventCreate(&c->t1) == cudaSuccess;
   if (ok && c->keep) ok = cudaMalloc(&c->raw, S * c->W * sizeof(float)) == cudaSuccess;
@@ -558,7 +592,7 @@ int hb_ingest(hb_ctx* c, const float* samples, int n, void* stream) {
     // gather columns [done, done+chunk) of every stream into the contiguous prefill buffer
     CK(c, cudaMemcpy2DAsync(c->prefill, sizeof(float) * chunk, samples + done, sizeof(float) * n,
                             sizeof(float) * chunk, S, cudaMemcpyHostToDevice, st));
-    CK(c, launch_ingest_window(c->prefill, c->ring, c->wpos, c->P, c->leads, chunk, c->R, c->W, nullptr, nullptr,
+    CK(c, launch_ingest_window(c->prefill, c->ring, c->wpos, c->P, c->leads, chunk, c->R, c->W, nullptr, 0, nullptr,
                                nullptr, st));
     CK(c, launch_advance(c->wpos, chunk, st));
     done += chunk;

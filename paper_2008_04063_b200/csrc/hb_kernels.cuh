@@ -56,6 +56,7 @@ struct ConvArgs {
   int relu;
   const float* fc_w;               // head: [G][cout] -> head_out[G*Pm][n_ntiles][mt_per_p] (null = no head)
   float* head_out;
+  size_t head_g_stride;            // floats between members' head partials (patient-chunked groups)
   int dbg;                         // experiments only (HB_DEBUG env)
   unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]
 };
@@ -75,7 +76,7 @@ struct ConvPlan {
 const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                       const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
                       const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
-                      float* head_out, int num_sms);
+                      float* head_out, int num_sms, size_t head_g_stride = 0);
 size_t bias_len(int cout);  // per-member bias floats (zero padded to whole N tiles)
 // Programmatic dependent launch on/off (HB_NO_PDL=1 disables).
 bool pdl_enabled();
@@ -126,7 +127,8 @@ cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int
 // raw gathered window [P][leads][window] fp32, stats (optional) mean/std.
 cudaError_t launch_ingest_window(const float* staged /*[P][leads][n_new]*/, float* ring /*[P][leads][R]*/,
                                  const long long* wpos, int P, int leads, int n_new, int R, int window,
-                                 __half* xn, float* raw_out, float* stats, cudaStream_t st);
+                                 __half* xn /*[leads][xn_rows][window]*/, int xn_rows, float* raw_out,
+                                 float* stats, cudaStream_t st);
 cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st);
 
 // head + ensemble aggregation: partial[m][P][mt] -> member logits, ensemble outputs.

@@ -124,3 +124,22 @@ def test_full_zoo_c3_matches_oracle():
     with EnsembleEngine(zoo, sel, P, hop=W) as eng:
         res = eng.tick(streams)
     _compare(res, *_oracle_tick(zoo, sel, streams, W))
+
+
+def test_patient_chunking_is_bit_identical(monkeypatch):
+    """Member chains over patient chunks (activation budget) give bit-identical results."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, C2)
+    P, W, hop = 7, 7500, 250
+    streams = _streams(P, W + hop, seed=12)
+    outs = []
+    for budget in (None, "0.05"):          # 50 MB forces chunks of 1-2 beds
+        if budget:
+            monkeypatch.setenv("HB_ACT_BUDGET_GB", budget)
+        with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+            eng.ingest(streams[:, :, :W - hop])
+            eng.tick(streams[:, :, W - hop:W])
+            outs.append(eng.tick(streams[:, :, W:W + hop]))
+    assert np.array_equal(outs[0].member_logits, outs[1].member_logits)
+    assert np.array_equal(outs[0].ens_prob, outs[1].ens_prob)
