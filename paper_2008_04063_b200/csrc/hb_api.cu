@@ -362,36 +362,36 @@ int build_selection(hb_ctx* c) {
     }
     __half* const* act = &c->act[3 * g.lane];
     for (int ch = 0; ch < c->n_chunks; ++ch) {
-    g.plan0.push_back(c->plans.size());
-    int cur = 0;
-    const int nblocks = static_cast<int>(g.layers.size() - 1) / 2;
-    for (size_t li = 1; li < g.layers.size(); ++li) {
-      const LayerSpec& L = g.layers[li];
-      const bool conv1 = (li % 2 == 1);
-      const int blk = static_cast<int>(li - 1) / 2;
-      int src = cur, dst, out_split = 0, res_len = 0;
-      const __half* res = nullptr;
-      if (conv1) {
-        dst = (cur + 1) % 3;
-      } else {
-        src = (cur + 1) % 3;
-        dst = (cur + 2) % 3;
-        res = act[cur];
-        res_len = g.layers[li - 1].lin;
-        // the output of an even block feeds the next (stride-2) block: parity-split layout
-        out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
+      g.plan0.push_back(c->plans.size());
+      int cur = 0;
+      const int nblocks = static_cast<int>(g.layers.size() - 1) / 2;
+      for (size_t li = 1; li < g.layers.size(); ++li) {
+        const LayerSpec& L = g.layers[li];
+        const bool conv1 = (li % 2 == 1);
+        const int blk = static_cast<int>(li - 1) / 2;
+        int src = cur, dst, out_split = 0, res_len = 0;
+        const __half* res = nullptr;
+        if (conv1) {
+          dst = (cur + 1) % 3;
+        } else {
+          src = (cur + 1) % 3;
+          dst = (cur + 2) % 3;
+          res = act[cur];
+          res_len = g.layers[li - 1].lin;
+          // the output of an even block feeds the next (stride-2) block: parity-split layout
+          out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
+        }
+        ConvPlan plan;
+        // head partials of chunk ch: rows [ch*Pc, (ch+1)*Pc) of every member's [P_pad][head_mt] block
+        float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
+        const char* e = plan_conv(&plan, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+                                  L.head ? nullptr : act[dst], out_split, g.wpack[li - 1], g.bias[li - 1], res,
+                                  conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr, head_base,
+                                  c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
+        if (e) return fail(c, HB_E_INVALID, e);
+        c->plans.push_back(plan);
+        if (!conv1) cur = dst;
       }
-      ConvPlan plan;
-      // head partials of chunk ch: rows [ch*Pc, (ch+1)*Pc) of every member's [P_pad][head_mt] block
-      float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
-      const char* e = plan_conv(&plan, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
-                                L.head ? nullptr : act[dst], out_split, g.wpack[li - 1], g.bias[li - 1], res,
-                                conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr, head_base,
-                                c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
-      if (e) return fail(c, HB_E_INVALID, e);
-      c->plans.push_back(plan);
-      if (!conv1) cur = dst;
-    }
     }
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
