@@ -177,6 +177,8 @@ const char* hb_curve_last_error(void);
 int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
                  int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
                  const float* fc_w_host, float* head_out, void* stream);
+/* M tiles per patient of a conv layer (head_out of hb_op_conv1d is [P][this]). */
+int hb_conv_mt(int cin, int cout, int lin, int stride, int head);
 /* Micro-benchmark of one conv layer shape on zero data: mean ms per launch. */
 int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out);
 int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,

@@ -71,6 +71,7 @@ _SIGS = {
     "hb_curve_last_error": (C.c_char_p, []),
     "hb_op_conv1d": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
                                C.c_int, _P, C.c_int, _F, _P, _P]),
+    "hb_conv_mt": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "hb_bench_conv": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
     "hb_op_stem": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, _P]),
 }

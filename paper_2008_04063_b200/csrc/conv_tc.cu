@@ -63,6 +63,102 @@ __device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile) {
   return t;
 }
 
+// Folded epilogue read: D'[r, (j, c)] holds folded tap j of output row r - j,
+// so out[r, c] = D'[r, (0, c)] + D'[r + 1, (1, c)] for F = 2.  Row r + 1 of the
+// same warp comes by shuffle; lane 31 takes row 32(w+1) from the next warp's
+// lane 0 through a small shared-memory exchange (one named barrier per round).
+constexpr int kXchRound = 3 * 32;            // [warp 0..2][32 channels]
+constexpr int kXchPerWg = 2 * kXchRound;     // double-buffered by round parity
+template <int F>
+__device__ __forceinline__ void fetch_round(uint32_t taddr, int bn, bool two, int wq, uint32_t lane, float* xch,
+                                            int eg, float* v, uint64_t* release) {
+  uint32_t r0[16], r1[16];
+  tmem_ld16_nw(taddr, r0);
+  if (two) tmem_ld16_nw(taddr + 16, r1);
+  if constexpr (F == 1) {
+    tmem_wait_ld();
+    if (release) {
+      tc_fence_before();
+      mbar_arrive(release);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r0[k]);
+    if (two) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[16 + k] = __uint_as_float(r1[k]);
+    }
+  } else {
+    uint32_t s0[16], s1[16];
+    tmem_ld16_nw(taddr + static_cast<uint32_t>(bn), s0);
+    if (two) tmem_ld16_nw(taddr + static_cast<uint32_t>(bn) + 16, s1);
+    tmem_wait_ld();
+    if (release) {
+      tc_fence_before();
+      mbar_arrive(release);
+    }
+    if (wq > 0 && lane == 0) {  // my row 0, folded block 1 -> the warp above
+      float* d = xch + (wq - 1) * 32;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) d[k] = __uint_as_float(s0[k]);
+      if (two) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) d[16 + k] = __uint_as_float(s1[k]);
+      }
+    }
+    named_bar_sync(1 + eg, 128);
+    const float* b = xch + (wq < 3 ? wq : 0) * 32;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float t = __shfl_down_sync(0xffffffffu, __uint_as_float(s0[k]), 1);
+      if (lane == 31) t = (wq < 3) ? b[k] : 0.f;
+      v[k] = __uint_as_float(r0[k]) + t;
+    }
+    if (two) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        float t = __shfl_down_sync(0xffffffffu, __uint_as_float(s1[k]), 1);
+        if (lane == 31) t = (wq < 3) ? b[16 + k] : 0.f;
+        v[16 + k] = __uint_as_float(r1[k]) + t;
+      }
+    }
+  }
+}
+
+// MMA issue for one k-chunk with `F` taps folded into N (warp-uniform walk,
+// one elected lane issues; two 64-bit descriptor adds per MMA).
+template <int F, typename ToffS2>
+__device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t& accum, int per_tap, uint32_t rows16,
+                                             uint32_t bstep16, uint32_t btap, ToffS2 toff_s2) {
+  for (int j = 0; j < per_tap; ++j) {
+    uint64_t bd = bdesc + static_cast<uint32_t>(j) * bstep16;
+    if (a.stride == 1) {
+      uint64_t ad = adesc + static_cast<uint32_t>(2 * j) * rows16 + static_cast<uint32_t>(-a.pad - a.row0);
+#pragma unroll
+      for (int q = 0; q < kTaps / F; ++q) {
+        if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+        accum = 1u;
+        ad += F;
+        bd += btap;
+      }
+    } else {
+      const uint64_t ag = adesc + static_cast<uint32_t>(2 * j) * rows16;
+      uint64_t a0 = ag + toff_s2(0), a1 = ag + toff_s2(1);
+#pragma unroll
+      for (int q = 0; q < kTaps / (2 * F); ++q) {
+        if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+        accum = 1u;
+        bd += btap;
+        if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+        bd += btap;
+        a0 += F;
+        a1 += F;
+      }
+    }
+  }
+}
+
+template <int F>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ ConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -79,6 +175,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   float* s_head = reinterpret_cast<float*>(tmem_holder + 4);  // [2][4] per-warp head partials
   float* s_bias = s_head + 8;                                  // [G][bn] when every N tile is whole
   float* s_fc = s_bias + a.sb_len;                             // [G][bn]
+  float* s_xch = s_fc + a.sb_len;                              // [2 wg][kXchPerWg] folded-row exchange
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -148,7 +245,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++li) {
         const TileIdx t = decode_tile(a, tile);
         const int p = t.p;
-        const int blk = (t.mt * kBM + a.row0) / 8;  // first 128-B line (8 rows)
+        const int blk = (t.mt * a.stride_m + a.row0) / 8;  // first 128-B line (8 rows)
         const int key = t.g * a.n_ntiles + t.nt;
         const bool load_b = !a.b_resident || key != loaded_key;
         // Reloading resident weights (next member of the group): the MMA warp
@@ -189,12 +286,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // -------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop with warp-uniform values (kept in uniform
     // registers); one elected lane issues each tcgen05.mma / commit.
-    const uint32_t idesc = make_idesc_f16(kBM, a.bn);
+    const uint32_t idesc = make_idesc_f16(kBM, a.bnp);
     const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
-    const uint32_t b_lbo = static_cast<uint32_t>(a.bn * 16);
+    const uint32_t b_lbo = static_cast<uint32_t>(a.bnp * 16);
     const uint32_t rows16 = static_cast<uint32_t>(a.rows);  // one group column, 16 B units
     const uint32_t region16 = region_bytes >> 4;           // one parity region
-    const uint32_t bstep16 = static_cast<uint32_t>(2 * a.bn);
+    const uint32_t bstep16 = static_cast<uint32_t>(2 * a.bnp);
     const int per_tap = a.ck >> 4;  // 0 for 8-channel chunks
     // stride-2 A offset (16 B units) of tap t in {0, 1}: parity region + pair row
     auto toff_s2 = [&](int t) -> uint32_t {
@@ -226,7 +323,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_wait(&acc_empty[acc], accph ^ 1, 10 + 1000 * static_cast<int>(bres_ph));
       if (prof) t_acc += clock64() - t0;
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bn);
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bnp);
       for (int kc = 0; kc < a.n_kchunks; ++kc) {
         const int slot = a.b_resident ? kc : bs;
         if (prof) t0 = clock64();
@@ -246,33 +343,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         // taps alternate parity regions, each advancing one row per tap pair.
         uint32_t accum = kc > 0 ? 1u : 0u;
         if (per_tap > 0) {
+          // K-steps are (tap group q, 16-channel sub-chunk j); a tap group is
+          // `fold` taps sharing one A view (s=1: taps qF..qF+F-1; s=2: taps of
+          // one parity, t0, t0+2, ..), their weights side by side in N.
           const uint32_t btap = static_cast<uint32_t>(per_tap) * bstep16;
-          for (int j = 0; j < per_tap; ++j) {
-            uint64_t bd = bdesc + static_cast<uint32_t>(j) * bstep16;
-            if (a.stride == 1) {
-              uint64_t ad = adesc + static_cast<uint32_t>(2 * j) * rows16 + static_cast<uint32_t>(-a.pad - a.row0);
-#pragma unroll
-              for (int t = 0; t < kTaps; ++t) {
-                if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
-                accum = 1u;
-                ad += 1;
-                bd += btap;
-              }
-            } else {
-              const uint64_t ag = adesc + static_cast<uint32_t>(2 * j) * rows16;
-              uint64_t a0 = ag + toff_s2(0), a1 = ag + toff_s2(1);
-#pragma unroll
-              for (int tp = 0; tp < kTaps / 2; ++tp) {
-                if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
-                accum = 1u;
-                bd += btap;
-                if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
-                bd += btap;
-                a0 += 1;
-                a1 += 1;
-              }
-            }
-          }
+          issue_groups<F>(a, d_tmem, adesc, bdesc, idesc, accum, per_tap, rows16, bstep16, btap, toff_s2);
         } else {
           // 8-channel chunk: one K-step pairs taps (t, t+1) [s=1] or (t, t+2) [s=2],
           // i.e. the same region one row apart (LBO = 16 B)
@@ -344,15 +419,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int res_groups = a.res_mode ? a.res_c / 8 : 0;
     const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0 && eg == 0;
     unsigned long long e_wait = 0, e_work = 0, et0 = 0, e_start = eprof ? clock64() : 0;
+    uint32_t xround = 0;  // exchange buffer parity, alternates every round across tiles
     pdl_wait();
     for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
       const TileIdx ti = decode_tile(a, tile);
       const int nt = ti.nt;
       const int p = ti.p;
       const int mt = ti.mt;
-      const int l = mt * kBM + r;
-      const bool valid = l < a.lout;
-      const bool in_buf = l < a.out_rows;
+      const int l = mt * a.stride_m + r;
+      const bool own = r < a.stride_m;  // rows past stride_m belong to the next tile (folded taps)
+      const bool valid = own && l < a.lout;
+      const bool in_buf = own && l < a.out_rows;
       const int g0 = nt * (a.bn / 8);
       const int ng = min(a.bn / 8, out_groups - g0);
       // Shortcut rows are independent of the accumulator: fetch the first 8
@@ -392,16 +469,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         et0 = t1;
       }
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(acc * a.bnp);
       float head = 0.f;
+      // Rounds of up to 32 output channels: all TMEM loads of a round are
+      // issued before one wait; after the last round's loads the accumulator
+      // is released, so the next tile's MMAs overlap this tile's math/stores.
+      const int nrounds = (ng + 3) >> 2;
 #pragma unroll
-      for (int c16 = 0; c16 < 16; ++c16) {
-        if (c16 * 2 >= ng) break;
-        float v[16];
-        tmem_ld16(taddr + static_cast<uint32_t>(c16 * 16), v);
+      for (int q = 0; q < 8; ++q) {  // unrolled: the shortcut registers are indexed statically
+        if (q >= nrounds) break;
+        const bool two = ng > 4 * q + 2;  // second 16-channel chunk in this round
+        float v[32];
+        fetch_round<F>(taddr + static_cast<uint32_t>(q * 32), a.bn, two, wq, lane,
+                       s_xch + eg * kXchPerWg + (xround++ & 1) * kXchRound, eg, v,
+                       q == nrounds - 1 ? &acc_empty[acc] : nullptr);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = 2 * c16 + h;
+        for (int h = 0; h < 4; ++h) {
+          const int j = 4 * q + h;
           if (j >= ng) break;
           const int g = g0 + j;
           float y[8];
@@ -453,8 +537,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[acc]);
       if (eprof) e_work += clock64() - et0;
       accph ^= 1;
       if (a.fc_w != nullptr) {
@@ -495,7 +577,33 @@ int conv_bn(int cout) {
 
 // barriers + holder/head scratch + per-member bias and fc (up to 1024 floats each)
 constexpr int kSmemBiasMax = 1024;
-constexpr uint32_t kFixedSmem = 1024 + 256 + 2 * kSmemBiasMax * 4;
+constexpr uint32_t kXchBytes = 2 * kXchPerWg * 4;  // folded-row exchange, both epilogue warpgroups
+// upper bound used for the k-chunk / residency decision (shared with the packer)
+constexpr uint32_t kFixedSmem = 1024 + 256 + 2 * kSmemBiasMax * 4 + kXchBytes;
+
+int conv_stride_m(int fold) { return fold > 1 ? 120 : kBM; }
+static int pick_ck(int cin, int cout, int stride, int* resident);
+
+// Taps folded into N: enough to lift a narrow layer off the shared-memory
+// bound (A is read once per tap group instead of once per tap) while
+// F*bn <= 256 (MMA N, and 2 TMEM accumulators <= 512 columns).  HB_FOLD
+// caps it (1 disables).  8-channel k-chunks keep their tap-pair K layout.
+int conv_fold(int cin, int cout, int stride) {
+  static const int cap = getenv("HB_FOLD") ? atoi(getenv("HB_FOLD")) : 1;  // off by default (see below)
+  int resident;
+  const int ck = pick_ck(cin, cout, stride, &resident);
+  const int bn = conv_bn(cout);
+  if (ck < 16 || round_up(cout, 16) > bn) return 1;  // (several N tiles: no fold)
+  // Measured (profiles/r01_fold_ab.txt): at bn = 32 the folded epilogue, not
+  // the MMA, bounds the tile; 64 -> 64 layers gain 4-8 % alone, wider or
+  // channel-doubling layers lose, and inside the two-branch tick graph even
+  // the 64 -> 64-only setting loses (1.212 vs 1.177 ms), so HB_FOLD=2 is an
+  // opt-in experiment.
+  if (bn != 64 || cin < 64) return 1;
+  int f = 1;
+  while (f * 2 <= cap && f * 2 <= 2 && f * 2 * bn <= 256) f *= 2;
+  return f;
+}
 
 static int a_rows(int stride) { return stride == 1 ? kRowsS1 : kRowsS2; }
 
@@ -548,32 +656,36 @@ void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) 
   const int ck = pick_ck(cin, cout, stride, &resident);
   if (ck == 0) return;
   const int nkc = cin / ck;
-  const int ksteps = (ck >= 16) ? ck : 8;
+  const int F = conv_fold(cin, cout, stride);
+  const int ksteps = (ck >= 16) ? ck / F : 8;  // K-steps per k-chunk
   size_t o = 0;
   for (int nt = 0; nt < nnt; ++nt)
     for (int kc = 0; kc < nkc; ++kc)
       for (int ks = 0; ks < ksteps; ++ks)
-        for (int half = 0; half < 2; ++half) {
-          int t, c0;
-          if (ck >= 16) {
-            const int per_tap = ck / 16;
-            t = ks / per_tap;
-            c0 = kc * ck + 16 * (ks % per_tap) + 8 * half;
-          } else {
-            const int t0 = (stride == 1) ? 2 * ks : (ks / 2) * 4 + (ks % 2);
-            t = t0 + half * stride;
-            c0 = kc * ck;
-          }
-          for (int n = 0; n < bn; ++n)
-            for (int j = 0; j < 8; ++j) {
-              const int co = nt * bn + n;
-              const float v = (co < cout) ? w[(static_cast<size_t>(co) * cin + (c0 + j)) * kTaps + t] : 0.f;
-              const __half hv = __float2half_rn(v);
-              uint16_t bits;
-              std::memcpy(&bits, &hv, 2);
-              dst[o++] = bits;
+        for (int half = 0; half < 2; ++half)
+          for (int jj = 0; jj < F; ++jj) {  // N rows: folded tap jj, then output channel
+            int t, c0;
+            if (ck >= 16) {
+              const int per_tap = ck / 16;
+              const int gi = ks / per_tap;  // tap group
+              const int base = (stride == 1) ? gi * F : (gi >> 1) * 2 * F + (gi & 1);
+              t = base + jj * stride;
+              c0 = kc * ck + 16 * (ks % per_tap) + 8 * half;
+            } else {
+              const int t0 = (stride == 1) ? 2 * ks : (ks / 2) * 4 + (ks % 2);
+              t = t0 + half * stride;
+              c0 = kc * ck;
             }
-        }
+            for (int n = 0; n < bn; ++n)
+              for (int j = 0; j < 8; ++j) {
+                const int co = nt * bn + n;
+                const float v = (co < cout) ? w[(static_cast<size_t>(co) * cin + (c0 + j)) * kTaps + t] : 0.f;
+                const __half hv = __float2half_rn(v);
+                uint16_t bits;
+                std::memcpy(&bits, &hv, 2);
+                dst[o++] = bits;
+              }
+          }
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -640,12 +752,17 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.ck = pick_ck(cin, cout, stride, &resident);
   if (a.ck == 0) return "conv: no k-chunk fits in shared memory";
   a.n_kchunks = cin / a.ck;
-  const int ksteps = (a.ck >= 16) ? a.ck : 8;
-  a.mt_per_p = (a.out_rows + kBM - 1) / kBM;
+  a.fold = conv_fold(cin, cout, stride);
+  a.bnp = a.fold * a.bn;
+  a.stride_m = conv_stride_m(a.fold);
+  const int ksteps = (a.ck >= 16) ? a.ck / a.fold : 8;
+  a.mt_per_p = (a.out_rows + a.stride_m - 1) / a.stride_m;
   a.num_tiles = a.n_ntiles * P * a.mt_per_p;
   a.a_stage_bytes = static_cast<uint32_t>(stride * (a.ck / 8) * a.rows * 16);
-  a.b_chunk_bytes = static_cast<uint32_t>(ksteps * 2 * a.bn * 16);
-  const uint32_t budget = kSmemLimit - kFixedSmem;
+  a.b_chunk_bytes = static_cast<uint32_t>(ksteps * 2 * a.bnp * 16);
+  a.sb_len = (a.n_ntiles == 1 && G * a.bn <= kSmemBiasMax) ? G * a.bn : 0;
+  const uint32_t fixed = 1024 + 256 + 2 * static_cast<uint32_t>(a.sb_len) * 4 + (a.fold > 1 ? kXchBytes : 0);
+  const uint32_t budget = kSmemLimit - fixed;
   const uint32_t b_all = a.b_chunk_bytes * a.n_kchunks;
   a.b_resident = resident;
   a.nb_slots = resident ? a.n_kchunks : 2;
@@ -656,13 +773,12 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   if (a.na_stages > max_stages) a.na_stages = max_stages;
   if (a.na_stages < 2) return "conv: k-chunk does not fit in shared memory";
   uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(2 * a.bn)) cols <<= 1;
+  while (cols < static_cast<uint32_t>(2 * a.bnp)) cols <<= 1;
   a.tmem_cols = cols;
   a.wpack = wpack;
   a.wpack_stride = wpack_bytes(cin, cout);
   a.bias = bias;
   a.bias_stride = static_cast<int>(bias_len(cout));
-  a.sb_len = (a.n_ntiles == 1 && G * a.bn <= kSmemBiasMax) ? G * a.bn : 0;
   a.out = out;
   a.res = res;
   a.res_mode = res ? res_mode : 0;
@@ -674,7 +790,7 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.head_out = head_out;
   a.head_g_stride = head_g_stride ? head_g_stride : static_cast<size_t>(Pm) * a.n_ntiles * a.mt_per_p;
   a.dbg = dbg;
-  plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + kFixedSmem;
+  plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + fixed;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
 
   EncodeTiledFn enc = get_encode();
@@ -704,7 +820,10 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
 }
 
 cudaError_t init_conv_kernel() {
-  return cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(conv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  return e;
 }
 
 cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st) {
@@ -718,7 +837,8 @@ cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv_tc_kernel, plan.tmap, plan.args);
+  if (plan.args.fold == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<2>, plan.tmap, plan.args);
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1>, plan.tmap, plan.args);
 }
 
 }  // namespace hb

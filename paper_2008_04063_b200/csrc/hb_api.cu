@@ -344,9 +344,10 @@ int build_selection(hb_ctx* c) {
       g.bias.push_back(b);
     }
     CK(c, cudaMalloc(&g.fc_w, sizeof(float) * c_last * G));
-    {  // head partials per (patient, N tile, M tile) of the last layer
-      const int cl = g.layers.back().cout, bn = conv_bn(cl);
-      g.head_mt = ((round_up(cl, 16) + bn - 1) / bn) * ((g.layers.back().lout + kBM - 1) / kBM);
+    {  // head partials per (patient, N tile, M tile) of the last layer, as that layer is tiled
+      const LayerSpec& H = g.layers.back();
+      const int bn = conv_bn(H.cout), sm = conv_stride_m(conv_fold(H.cin, H.cout, H.stride));
+      g.head_mt = ((round_up(H.cout, 16) + bn - 1) / bn) * ((H.lout + sm - 1) / sm);
     }
     CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P_pad * g.head_mt));
     g.stem.assign(c->n_chunks, {});
@@ -389,6 +390,8 @@ int build_selection(hb_ctx* c) {
                                   conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr, head_base,
                                   c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
         if (e) return fail(c, HB_E_INVALID, e);
+        if (L.head && plan.args.n_ntiles * plan.args.mt_per_p != g.head_mt)
+          return fail(c, HB_E_INVALID, "head tiling mismatch");
         c->plans.push_back(plan);
         if (!conv1) cur = dst;
       }
@@ -817,6 +820,14 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
   cudaFree(db);
   cudaFree(dfc);
   return rc;
+}
+
+int hb_conv_mt(int cin, int cout, int lin, int stride, int head) {
+  const int lout = (lin + stride - 1) / stride;
+  const int rows = head ? lout : act_rows(lout, 0);
+  const int sm = conv_stride_m(conv_fold(cin, cout, stride));
+  const int bn = conv_bn(cout), nnt = (round_up(cout, 16) + bn - 1) / bn;
+  return (head ? nnt : 1) * ((rows + sm - 1) / sm);
 }
 
 int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out) {

@@ -35,6 +35,7 @@ inline int act_rows(int L, int split) { return split ? 2 * lh_S(L) : lp_I(L); }
 struct ConvArgs {
   int P, cin, cout, bn, n_ntiles;  // P = G*Pm rows of the activation tensors; bn = per-tile N (mult of 16, <=256)
   int G, Pm;                       // members sharing this layer shape (one launch), patients per member
+  int fold, bnp, stride_m;         // taps folded into N (D' = [128 x fold*bn]), MMA N, output rows per M tile
   int lin, lout;
   int out_split, out_lp, out_lh;   // output layout (I: out_lp rows; S: 2 x out_lh rows)
   int out_rows;                    // positions that must be written (valid or zero padding)
@@ -78,6 +79,8 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
                       const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
                       float* head_out, int num_sms, size_t head_g_stride = 0);
 size_t bias_len(int cout);  // per-member bias floats (zero padded to whole N tiles)
+int conv_fold(int cin, int cout, int stride);  // taps folded into the MMA N dimension (1, 2 or 4)
+int conv_stride_m(int fold);                   // output rows per M tile (128, or 120 when folded)
 // Programmatic dependent launch on/off (HB_NO_PDL=1 disables).
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>

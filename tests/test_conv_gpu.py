@@ -56,9 +56,8 @@ def run_conv(x, w, b, stride, res=None, res_mode=0, fc_w=None, out_split=0):
     rin = None
     if res is not None:
         rin = to_split(res.to(dev)) if res_mode == 2 else to_ng8(res.to(dev))
-    c16 = (max(cout, 16) + 15) // 16 * 16
-    n_nt = 1 if c16 <= 256 else -(-c16 // 256)              # N tiles (conv_bn in conv_tc.cu)
-    head = torch.zeros(P, n_nt * ((lout + 127) // 128), dtype=torch.float32, device=dev) if fc_w is not None else None
+    mt = L.lib().hb_conv_mt(cin, cout, lin, stride, 1)       # [N tiles x M tiles] head partials
+    head = torch.zeros(P, mt, dtype=torch.float32, device=dev) if fc_w is not None else None
     wn = np.ascontiguousarray(w.numpy(), np.float32)
     bn = np.ascontiguousarray(b.numpy(), np.float32)
     fcn = np.ascontiguousarray(fc_w.numpy(), np.float32) if fc_w is not None else None
