@@ -177,12 +177,24 @@ const char* hb_curve_last_error(void);
 int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
                  int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
                  const float* fc_w_host, float* head_out, void* stream);
+/* General form: every layout is Q-phase (hb_kernels.cuh: per 8-channel plane,
+ * Q phase sub-planes of roundup(ceil(L/Q), 8) rows, position l at phase l%Q,
+ * row l/Q; I = Q1, S = Q2).  kind: 0 = K4 (positions on M; input Q = stride),
+ * 1 = K4b polyphase (output phases x channels on M; input Q = stride*128/cout,
+ * no fused head), -1 = the serving planner's choice (hb_conv_kind). */
+int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
+                   int cout, const void* res, int res_mode, int res_c, int res_len, int res_q, void* out, int out_q,
+                   const float* fc_w_host, float* head_out, int kind, void* stream);
+int hb_conv_kind(int cin, int cout, int stride, int head);
 /* M tiles per patient of a conv layer (head_out of hb_op_conv1d is [P][this]). */
 int hb_conv_mt(int cin, int cout, int lin, int stride, int head);
 /* Micro-benchmark of one conv layer shape on zero data: mean ms per launch. */
 int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out);
+int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode, int kind, int iters, float* ms_out);
 int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
                void* stream);
+int hb_op_stem_q(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
+                 int out_q, void* stream);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,11 @@ _SIGS = {
     "hb_conv_mt": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "hb_bench_conv": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
     "hb_op_stem": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, _P]),
+    "hb_op_conv1d_q": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
+                                 C.c_int, C.c_int, _P, C.c_int, _F, _P, C.c_int, _P]),
+    "hb_conv_kind": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "hb_bench_conv_k": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
+    "hb_op_stem_q": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, _P]),
 }
 
 _lock = threading.Lock()

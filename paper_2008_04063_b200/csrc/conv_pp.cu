@@ -1,0 +1,495 @@
+// K4b: polyphase implicit-GEMM conv1d for narrow layers (C_out in {16, 32, 64},
+// C_in in {16, 32, 64}; 16 taps, stride 1|2, "same" padding) on tcgen05, with
+// bias / shortcut (identity or maxpool(2), zero-padded channels) / ReLU fused
+// into the TMEM epilogue.
+//
+// Why a second conv kernel.  K4 (conv_tc.cu) puts 128 output positions on the
+// UMMA M side and C_out on N.  For C_out = 32 every 128x32x16 MMA then reads a
+// 4 KB A slice + 1 KB B slice from shared memory for 16 cycles of math: the
+// layer runs at the shared-memory read rate (~45 cycles per MMA, 35-40 % of
+// the tensor peak, profiles/r01_convbench.txt).  Here the roles swap and the
+// M side is filled with output PHASES:
+//
+//   ph = 128 / C_out output phases, Q = stride * ph input phases,
+//   Y[c, ph*n + p] = sum_{ci, t} W[c, ci, t] X[ci, Q*n + (stride*p + t) - pad]
+//   D[(p', c), n]  = sum_{u, ci} A[(p', c), (u, ci)] B[n, (u, ci)]     (p' = ph-1-p)
+//   A[(p', c), (u, ci)] = W[c, ci, u - stride*p]  (zero outside the 16 taps)
+//   B[n, (u, ci)]       = X[ci, Q*n + u - pad],   u in [0, U), U = stride*(ph-1) + 16
+//
+// so one MMA is M=128 (all phases x all output channels) x N=nb (up to 256
+// output columns) x K=16 (one shift u, 16 input channels): per 128x256x16 MMA
+// the shared-memory traffic is 4 KB (A) + 8 KB (B) for 128 cycles of math.
+// The zero taps cost U/16 - 1 of the MMA work (19/16 for C_out=32, s=1).
+//
+// Both operands are addressed without materialising anything:
+//  * A: per (input-channel half, tap parity) the weights are stored as a
+//    padded tap array [ph-1 zeros, taps, ph-1 zeros] of C_out x 16 B rows.
+//    M row (p', c) of shift u is array entry (u - pi)/s + p' at row c, i.e.
+//    the 128 rows of the A slice are 128 CONSECUTIVE 16-B rows starting at
+//    entry (u - pi)/s: a canonical K-major no-swizzle tile (SBO = 128 B)
+//    whose start address slides by one tap per shift.  Resident in smem.
+//  * B: the input is stored in the Q-phase layout (hb_kernels.cuh), so
+//    position Q*n + v lives in phase plane v mod Q at row n + floor(v/Q):
+//    for a fixed shift the N rows are consecutive 16-B rows of one phase
+//    plane.  One TMA box per (tile, 16-channel pair) brings every phase of
+//    the tile's row range; shift u is a descriptor offset.
+//
+// Roles (384 threads, 1 CTA/SM, persistent over tiles) as in K4: warp 0 TMA
+// producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 / 8-11 two
+// epilogue warpgroups (one per TMEM accumulator).  Epilogue thread r holds M
+// row r = (p', c) for nb columns; an 8x8 register transpose by warp shuffles
+// inside each 8-lane group turns that into 8 channels x one position per
+// lane, so the shortcut read and the output store are 16-byte rows.
+#include "hb_kernels.cuh"
+#include "hb_ptx.cuh"
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace hb {
+
+struct PPTile {
+  int g, p, nt;  // member of the group, global patient row [G*Pm], column tile
+};
+__device__ __forceinline__ PPTile pp_tile(const PPArgs& a, int tile) {
+  const int per_g = a.Pm * a.nt_per_p;
+  PPTile t;
+  t.g = tile / per_g;
+  int rem = tile - t.g * per_g;
+  const int pl = rem / a.nt_per_p;
+  t.nt = rem - pl * a.nt_per_p;
+  t.p = t.g * a.Pm + pl;
+  return t;
+}
+
+// 8x8 transpose inside aligned 8-lane groups: lane r8 holds row r8 (its
+// channel) at 8 columns; afterwards it holds column r8 across the 8 channels.
+__device__ __forceinline__ void transpose8(float (&v)[8], int r8) {
+#pragma unroll
+  for (int m = 4; m >= 1; m >>= 1) {
+    const bool hi = (r8 & m) != 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k & m) continue;
+      const float send = hi ? v[k] : v[k | m];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, m);
+      if (hi) v[k] = recv; else v[k | m] = recv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+    conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ PPArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sW = smem;
+  uint8_t* sB = smem + a.w_bytes;
+  uint64_t* st_full = reinterpret_cast<uint64_t*>(sB + static_cast<size_t>(a.n_stages) * a.stage_bytes);
+  uint64_t* st_empty = st_full + a.n_stages;
+  uint64_t* w_full = st_empty + a.n_stages;
+  uint64_t* w_empty = w_full + 1;
+  uint64_t* acc_full = w_empty + 1;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);  // [G][cout]
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmB);
+    for (int i = 0; i < a.n_stages; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    mbar_init(w_full, 1);
+    mbar_init(w_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
+  for (int i = threadIdx.x; i < a.G * a.cout; i += blockDim.x) {
+    const int g = i / a.cout;
+    s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------------------------------------------- producer
+      auto load_w = [&](int g) {
+        const uint8_t* src = a.wimg + static_cast<size_t>(g) * a.w_stride;
+        mbar_arrive_expect_tx(w_full, a.w_bytes);
+        for (uint32_t off = 0; off < a.w_bytes; off += 32768u) {
+          const uint32_t n = (a.w_bytes - off) < 32768u ? (a.w_bytes - off) : 32768u;
+          bulk_load(sW + off, src + off, n, w_full);
+        }
+      };
+      int loaded_g = -1, reloads = 0;
+      if (static_cast<int>(blockIdx.x) < a.num_tiles) {  // weights are immutable: before the dependency wait
+        loaded_g = pp_tile(a, blockIdx.x).g;
+        load_w(loaded_g);
+      }
+      pdl_wait();
+      int st = 0;
+      uint32_t sph = 0;
+      const int planes_per_p = a.cin / 8;
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+        const PPTile t = pp_tile(a, tile);
+        if (t.g != loaded_g) {  // next member of the group: wait until the MMAs on the old weights retired
+          mbar_wait(w_empty, static_cast<uint32_t>(reloads++) & 1u, 101);
+          load_w(t.g);
+          loaded_g = t.g;
+        }
+        const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
+        for (int j = 0; j < a.n_pairs; ++j) {
+          mbar_wait(&st_empty[st], sph ^ 1u, 102);
+          mbar_arrive_expect_tx(&st_full[st], a.stage_bytes);
+          tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmB, &st_full[st], 0, line0, 0,
+                      t.p * planes_per_p + 2 * j);
+          if (++st == a.n_stages) {
+            st = 0;
+            sph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = make_idesc_f16(kBM, a.nb);
+    const uint32_t b_lbo = static_cast<uint32_t>(a.Q * a.R * 16);
+    int st = 0;
+    uint32_t sph = 0;
+    int acc = 0;
+    uint32_t accph = 0;
+    uint32_t wph = 0;
+    int cur_g = static_cast<int>(blockIdx.x) < a.num_tiles ? pp_tile(a, blockIdx.x).g : 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const PPTile t = pp_tile(a, tile);
+      if (t.g != cur_g) {
+        wph ^= 1u;
+        cur_g = t.g;
+      }
+      mbar_wait(w_full, wph, 111);
+      mbar_wait(&acc_empty[acc], accph ^ 1u, 112);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.nb);
+      for (int j = 0; j < a.n_pairs; ++j) {
+        mbar_wait(&st_full[st], sph, 113);
+        tc_fence_after();
+        const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
+        const uint64_t b0 = make_desc(smem_u32(sB + static_cast<size_t>(st) * a.stage_bytes), b_lbo, 128);
+        for (int u = 0; u < a.U; ++u) {
+          const int pi = (a.stride == 2) ? (u & 1) : 0;
+          const uint32_t aoff = static_cast<uint32_t>(pi) * a.w_par16 +
+                                static_cast<uint32_t>((u - pi) >> (a.stride - 1)) * static_cast<uint32_t>(a.cout);
+          const int v = u - a.pad;
+          const uint32_t boff = static_cast<uint32_t>((v & (a.Q - 1)) * a.R + 8 + (v >> a.qs));
+          if (elect_one()) mma_f16_ss(d_tmem, a0 + aoff, b0 + boff, idesc, (j | u) ? 1u : 0u);
+        }
+        __syncwarp();
+        if (elect_one()) mma_commit(&st_empty[st]);
+        __syncwarp();
+        if (++st == a.n_stages) {
+          st = 0;
+          sph ^= 1u;
+        }
+      }
+      if (elect_one()) mma_commit(&acc_full[acc]);
+      __syncwarp();
+      const int nxt = tile + static_cast<int>(gridDim.x);
+      if (nxt < a.num_tiles && pp_tile(a, nxt).g != t.g) {  // the weights change after this tile
+        if (elect_one()) mma_commit(w_empty);
+        __syncwarp();
+      }
+      if (++acc == 2) {
+        acc = 0;
+        accph ^= 1u;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue
+    const int eg = (static_cast<int>(warp) - 4) >> 2;
+    const int wq = static_cast<int>(warp) & 3;
+    const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
+    const int pprime = row / a.cout;
+    const int c = row - pprime * a.cout;
+    const int phase = a.ph - 1 - pprime;
+    const int g8 = c >> 3;
+    const int r8 = static_cast<int>(lane) & 7;
+    const bool has_res = a.res_mode != 0 && g8 * 8 < a.res_c;
+    const int out_groups = a.cout / 8;
+    const int res_groups = a.res_c / 8;
+    uint32_t accph = 0;
+    pdl_wait();
+    for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+      const PPTile t = pp_tile(a, tile);
+      const float bias = s_bias[t.g * a.cout + c];
+      const size_t out_plane = static_cast<size_t>(t.p) * out_groups + g8;
+      const size_t res_plane = static_cast<size_t>(t.p) * res_groups + g8;
+      const int n_base = t.nt * a.nb + r8;  // + 32*ch + 8*b: this lane's column after the transpose
+      // Shortcut rows of a 32-column chunk (4 positions per lane after the
+      // transpose; maxpool reads 2 rows each) are loaded one chunk ahead, the
+      // first chunk before the accumulator wait, so their latency hides under
+      // the MMAs / the previous chunk's math.
+      uint4 raw[8];
+      auto load_res = [&](int ch) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int l = a.ph * (n_base + 32 * ch + 8 * b) + phase;
+          const bool ok = has_res && l < a.lout;
+          if (a.res_mode == 2) {
+            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l)))
+                            : make_uint4(0u, 0u, 0u, 0u);
+            raw[2 * b + 1] = ok ? __ldg(reinterpret_cast<const uint4*>(
+                                      a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1)))
+                                : make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l)))
+                            : make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+      };
+      if (a.res_mode) load_res(0);
+      mbar_wait(&acc_full[eg], accph, 120);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eg * a.nb);
+      const int nch = a.nb / 32;
+      for (int ch = 0; ch < nch; ++ch) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 32), r0);
+        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 32 + 16), r1);
+        uint4 rv[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (a.res_mode == 2) {
+            const __half2* h0 = reinterpret_cast<const __half2*>(&raw[2 * b]);
+            const __half2* h1 = reinterpret_cast<const __half2*>(&raw[2 * b + 1]);
+            __half2* o2 = reinterpret_cast<__half2*>(&rv[b]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o2[k] = __hmax2(h0[k], h1[k]);
+          } else {
+            rv[b] = a.res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        if (a.res_mode && ch + 1 < nch) load_res(ch + 1);
+        tmem_wait_ld();
+        if (ch == nch - 1) {  // accumulator drained: the next tile's MMAs may start
+          tc_fence_before();
+          mbar_arrive(&acc_empty[eg]);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          float v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t bits = (b < 2) ? r0[8 * b + k] : r1[8 * (b - 2) + k];
+            v[k] = __uint_as_float(bits) + bias;
+          }
+          transpose8(v, r8);
+          const int l = a.ph * (n_base + 32 * ch + 8 * b) + phase;
+          if (l < a.out_rows) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&rv[b]);
+            uint4 pk;
+            __half2* o2 = reinterpret_cast<__half2*>(&pk);
+            const bool valid = l < a.lout;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __half22float2(h2[k]);
+              const float y0 = fmaxf(v[2 * k] + f.x, 0.f);
+              const float y1 = fmaxf(v[2 * k + 1] + f.y, 0.f);
+              o2[k] = valid ? __floats2half2_rn(y0, y1) : __floats2half2_rn(0.f, 0.f);
+            }
+            *reinterpret_cast<uint4*>(a.out + q_off(out_plane, a.out_qs, a.out_lq, l)) = pk;
+          }
+        }
+      }
+      accph ^= 1u;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, a.tmem_cols);
+}
+
+// ------------------------------------------------------------------ host side
+
+int pp_phases(int cout) { return kBM / cout; }
+
+static int pp_taps_per_parity(int cout, int stride) { return kTaps / stride + 2 * (pp_phases(cout) - 1); }
+
+bool pp_shape_ok(int cin, int cout, int stride) {
+  if (cout != 16 && cout != 32 && cout != 64) return false;
+  if (cin != 16 && cin != 32 && cin != 64) return false;
+  return stride == 1 || stride == 2;
+}
+
+size_t pp_wbytes(int cin, int cout, int stride) {
+  return static_cast<size_t>(cin / 8) * stride * pp_taps_per_parity(cout, stride) * cout * 16;
+}
+
+// Weight image [pair j][half h][parity pi][entry e][cout][8 fp16]:
+// entry e of parity pi holds tap stride*(e - (ph-1)) + pi (zero outside [0,16)),
+// channels 16j + 8h .. +7.
+void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) {
+  const int ph = pp_phases(cout), na = pp_taps_per_parity(cout, stride);
+  size_t o = 0;
+  for (int j = 0; j < cin / 16; ++j)
+    for (int h = 0; h < 2; ++h)
+      for (int pi = 0; pi < stride; ++pi)
+        for (int e = 0; e < na; ++e) {
+          const int t = stride * (e - (ph - 1)) + pi;
+          for (int co = 0; co < cout; ++co)
+            for (int k = 0; k < 8; ++k) {
+              const int ci = 16 * j + 8 * h + k;
+              const float v = (t >= 0 && t < kTaps) ? w[(static_cast<size_t>(co) * cin + ci) * kTaps + t] : 0.f;
+              const __half hv = __float2half_rn(v);
+              uint16_t bits;
+              std::memcpy(&bits, &hv, 2);
+              dst[o++] = bits;
+            }
+        }
+}
+
+using EncodeTiledFnPP = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFnPP get_encode_pp() {
+  static EncodeTiledFnPP fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFnPP>(p);
+  }
+  return fn;
+}
+
+// Columns per tile: the largest N whose operands fit with >= 2 stages, then
+// the one that minimises (waves x per-tile cost) -- small layers at serving
+// batch sizes prefer narrower tiles over a ragged last wave.  HB_PP_NB forces.
+static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const int* fits) {
+  static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
+  const int cands[3] = {256, 128, 64};
+  const double cost[3] = {1.0, 1.08, 1.3};  // per-column cost of a narrower MMA (smem-read bound below 256)
+  int best = 0;
+  double best_t = 1e30;
+  for (int k = 0; k < 3; ++k) {
+    const int nb = cands[k];
+    if (!fits[k]) continue;
+    if (force && nb != force) continue;
+    const long tiles = static_cast<long>(tiles_per_col_unit) * ((n_cols + nb - 1) / nb);
+    const long waves = (tiles + num_sms - 1) / num_sms;
+    const double tt = static_cast<double>(waves) * nb * cost[k];
+    if (tt < best_t - 1e-9) {
+      best_t = tt;
+      best = nb;
+    }
+  }
+  return best;
+}
+
+const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
+                    const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms) {
+  std::memset(plan, 0, sizeof(*plan));
+  if (G < 1 || G > kMaxGroup || Pm < 1) return "conv_pp: bad group shape";
+  if (!pp_shape_ok(cin, cout, stride)) return "conv_pp: unsupported layer shape";
+  if (lout != (lin + stride - 1) / stride) return "conv_pp: lout must be ceil(lin/stride)";
+  if (pad < 0 || pad > 8) return "conv_pp: padding out of range";
+  if (out_q < 1 || out_q > 32 || (out_q & (out_q - 1))) return "conv_pp: out_q must be a power of two <= 32";
+  if (res && (res_q < 1 || res_q > 32 || (res_q & (res_q - 1)))) return "conv_pp: res_q must be a power of two <= 32";
+  if (res && res_c > cout) return "conv_pp: shortcut wider than the output";
+  PPArgs& a = plan->args;
+  a.G = G;
+  a.Pm = Pm;
+  a.P = G * Pm;
+  a.cin = cin;
+  a.cout = cout;
+  a.stride = stride;
+  a.pad = pad;
+  a.lin = lin;
+  a.lout = lout;
+  a.ph = pp_phases(cout);
+  a.Q = stride * a.ph;
+  a.qs = ilog2(a.Q);
+  a.U = stride * (a.ph - 1) + kTaps;
+  a.n_pairs = cin / 16;
+  const int na = pp_taps_per_parity(cout, stride);
+  a.w_par16 = static_cast<uint32_t>(na * cout);  // one parity array, 16-B units
+  a.w_half_bytes = static_cast<uint32_t>(stride * na * cout * 16);
+  a.w_pair_bytes = 2 * a.w_half_bytes;
+  a.w_bytes = static_cast<uint32_t>(pp_wbytes(cin, cout, stride));
+  a.w_stride = pp_wbytes(cin, cout, stride);
+  a.in_lq = lq_Q(lin, a.Q);
+  a.out_qs = ilog2(out_q);
+  a.out_lq = lq_Q(lout, out_q);
+  a.out_rows = act_rows_q(lout, out_q);
+  const int n_cols = (a.out_rows + a.ph - 1) / a.ph;
+  const int dr_max = (a.U - 1 - pad) >> a.qs;
+  const uint32_t fixed = 1024 + static_cast<uint32_t>(G * cout) * 4 + 256;
+  if (a.w_bytes + fixed >= kSmemLimit) return "conv_pp: weights do not fit in shared memory";
+  const uint32_t budget = kSmemLimit - fixed - a.w_bytes;
+  int fits[3];
+  const int cands[3] = {256, 128, 64};
+  for (int k = 0; k < 3; ++k) {
+    const int R = round_up(8 + cands[k] + dr_max, 8);
+    fits[k] = (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
+  }
+  a.nb = pick_nb(a.P, n_cols, num_sms, fits);
+  if (!a.nb) return "conv_pp: no column tile fits in shared memory";
+  a.R = round_up(8 + a.nb + dr_max, 8);
+  a.stage_bytes = static_cast<uint32_t>(2 * a.Q * a.R * 16);
+  a.n_stages = static_cast<int>(budget / a.stage_bytes);
+  if (a.n_stages > 4) a.n_stages = 4;
+  a.nt_per_p = (n_cols + a.nb - 1) / a.nb;
+  a.num_tiles = a.P * a.nt_per_p;
+  a.tmem_cols = static_cast<uint32_t>(2 * a.nb < 32 ? 32 : 2 * a.nb);
+  a.wimg = wimg;
+  a.bias = bias;
+  a.bias_stride = static_cast<int>(bias_len(cout));
+  a.out = out;
+  a.res = res;
+  a.res_mode = res ? res_mode : 0;
+  a.res_c = res ? res_c : 0;
+  a.res_qs = res ? ilog2(res_q) : 0;
+  a.res_lq = res ? lq_Q(res_len, res_q) : 0;
+  if (a.res && a.res_mode == 2 && act_rows_q(res_len, res_q) < 2 * lout)
+    return "conv_pp: maxpool shortcut shorter than the output";
+  plan->smem_bytes = a.w_bytes + a.n_stages * a.stage_bytes + fixed;
+  plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
+
+  EncodeTiledFnPP enc = get_encode_pp();
+  if (!enc) return "conv_pp: cuTensorMapEncodeTiled unavailable";
+  // input, Q-phase layout: {64 elems = one 128-B line of 8 rows, lq/8 lines, Q phases, P*cin/8 planes}
+  const cuuint64_t lq = static_cast<cuuint64_t>(a.in_lq);
+  const cuuint64_t dims[4] = {64, lq / 8, static_cast<cuuint64_t>(a.Q), static_cast<cuuint64_t>(a.P) * (cin / 8)};
+  const cuuint64_t strides[3] = {128, lq * 16, static_cast<cuuint64_t>(a.Q) * lq * 16};
+  const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(a.R / 8), static_cast<cuuint32_t>(a.Q), 2};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult rc = enc(&plan->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(in), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return "conv_pp: cuTensorMapEncodeTiled rejected the activation view";
+  return nullptr;
+}
+
+cudaError_t init_pp_kernel() {
+  return cudaFuncSetAttribute(conv_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+}
+
+cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st) {
+  return launch_pdl(conv_pp_kernel, dim3(plan.grid), dim3(kConvThreads), plan.smem_bytes, st, plan.tmap, plan.args);
+}
+
+}  // namespace hb

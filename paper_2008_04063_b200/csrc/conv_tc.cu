@@ -40,9 +40,22 @@ constexpr int kRowsS2 = 144;  // A rows per (parity, group) for stride 2 (18 lin
 __host__ __device__ __forceinline__ int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
 __device__ __forceinline__ size_t out_offset(const ConvArgs& a, int p, int g, int l) {
-  const size_t plane = static_cast<size_t>(p) * (a.cout / 8) + g;
-  if (!a.out_split) return (plane * a.out_lp + l) * 8;
-  return ((plane * 2 + (l & 1)) * a.out_lh + (l >> 1)) * 8;
+  return q_off(static_cast<size_t>(p) * (a.cout / 8) + g, a.out_qs, a.out_lq, l);
+}
+
+// Shortcut source row for output position l: identity x[l], or maxpool(2)
+// max(x[2l], x[2l+1]); x in its own Q-phase layout.
+__device__ __forceinline__ uint4 res_row(const ConvArgs& a, size_t plane, int l) {
+  if (a.res_mode == 1) return __ldg(reinterpret_cast<const uint4*>(a.res + q_off(plane, a.res_qs, a.res_lq, l)));
+  const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(a.res + q_off(plane, a.res_qs, a.res_lq, 2 * l)));
+  const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(a.res + q_off(plane, a.res_qs, a.res_lq, 2 * l + 1)));
+  uint4 o;
+  const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
+  const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
+  __half2* o2 = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o2[k] = __hmax2(h0[k], h1[k]);
+  return o;
 }
 
 // Tile order: member g of the group (slowest), N tile, patient, M tile.
@@ -442,18 +455,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         rres[j] = make_uint4(0u, 0u, 0u, 0u);
         const int g = g0 + j;
         if (j < ng && g < res_groups && valid) {
-          const size_t plane = static_cast<size_t>(p) * res_groups + g;
-          if (a.res_mode == 1) {
-            rres[j] = __ldg(reinterpret_cast<const uint4*>(a.res + (plane * a.res_rows + l) * 8));
-          } else {
-            const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2) * a.res_rows + l) * 8));
-            const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2 + 1) * a.res_rows + l) * 8));
-            const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
-            const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
-            __half2* o = reinterpret_cast<__half2*>(&rres[j]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) o[k] = __hmax2(h0[k], h1[k]);
-          }
+          rres[j] = res_row(a, static_cast<size_t>(p) * res_groups + g, l);
         }
       }
       const float* bias_t = smem_bias ? s_bias + ti.g * a.bn
@@ -496,19 +498,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (j < 8) {
               rv = rres[j < 8 ? j : 0];
             } else {
-              const size_t plane = static_cast<size_t>(p) * res_groups + g;
-              if (a.res_mode == 1) {
-                rv = __ldg(reinterpret_cast<const uint4*>(a.res + (plane * a.res_rows + l) * 8));
-              } else {
-                const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2) * a.res_rows + l) * 8));
-                const uint4 r1 =
-                    __ldg(reinterpret_cast<const uint4*>(a.res + ((plane * 2 + 1) * a.res_rows + l) * 8));
-                const __half2* h0 = reinterpret_cast<const __half2*>(&r0);
-                const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
-                __half2* o = reinterpret_cast<__half2*>(&rv);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) o[k] = __hmax2(h0[k], h1[k]);
-              }
+              rv = res_row(a, static_cast<size_t>(p) * res_groups + g, l);
             }
             const __half2* h2 = reinterpret_cast<const __half2*>(&rv);
 #pragma unroll
@@ -715,8 +705,8 @@ bool pdl_enabled() {
 }
 
 const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
-                      const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
-                      const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
+                      const __half* in, __half* out, int out_q, const uint8_t* wpack, const float* bias,
+                      const __half* res, int res_mode, int res_c, int res_len, int res_q, const float* fc_w,
                       float* head_out, int num_sms, size_t head_g_stride) {
   std::memset(plan, 0, sizeof(*plan));
   if (G < 1 || G > kMaxGroup || Pm < 1) return "conv: bad group shape";
@@ -734,10 +724,11 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.n_ntiles = (round_up(cout, 16) + a.bn - 1) / a.bn;
   a.lin = lin;
   a.lout = lout;
-  a.out_split = out_split;
-  a.out_lp = lp_I(lout);
-  a.out_lh = lh_S(lout);
-  a.out_rows = fc_w ? lout : act_rows(lout, out_split);
+  if (out_q < 1 || out_q > 32 || (out_q & (out_q - 1))) return "conv: out_q must be a power of two <= 32";
+  if (res && (res_q < 1 || res_q > 32 || (res_q & (res_q - 1)))) return "conv: res_q must be a power of two <= 32";
+  a.out_qs = ilog2(out_q);
+  a.out_lq = lq_Q(lout, out_q);
+  a.out_rows = fc_w ? lout : act_rows_q(lout, out_q);
   a.stride = stride;
   a.pad = pad;
   a.rows = a_rows(stride);
@@ -783,8 +774,10 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.res = res;
   a.res_mode = res ? res_mode : 0;
   a.res_c = res_c;
-  a.res_rows = (res_mode == 2) ? lh_S(res_len) : lp_I(res_len);
-  if (a.res && a.res_mode == 2 && lh_S(res_len) * 2 < 2 * lout) return "conv: maxpool shortcut shorter than the output";
+  a.res_qs = res ? ilog2(res_q) : 0;
+  a.res_lq = res ? lq_Q(res_len, res_q) : 0;
+  if (a.res && a.res_mode == 2 && act_rows_q(res_len, res_q) < 2 * lout)
+    return "conv: maxpool shortcut shorter than the output";
   a.relu = 1;
   a.fc_w = fc_w;
   a.head_out = head_out;

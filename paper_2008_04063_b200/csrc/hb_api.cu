@@ -48,10 +48,45 @@ std::vector<LayerSpec> member_layers(int width, int depth, int window) {
   return v;
 }
 
+// Conv kernel per layer: K4 (positions on M, conv_tc.cu) or K4b (output
+// phases x channels on M, conv_pp.cu) for the narrow layers it supports.
+// Measured per shape (profiles/r01_convbench_pp.txt) K4b wins 1.2-2.4x on
+// every supported shape at 1024 beds; at 64 beds it loses a few percent on
+// some small 64-channel launches in isolation, but inside the two-branch tick
+// graph sending every supported layer to K4b is fastest (c2 0.947 vs 0.958 ms
+// with a size rule, profiles/r01_pp_ab.txt).  HB_PP=0 keeps every layer on K4.
+enum { KIND_TC = 0, KIND_PP = 1 };
+bool pp_eligible(const LayerSpec& L) { return !L.head && L.cin >= 16 && pp_shape_ok(L.cin, L.cout, L.stride); }
+int layer_kind(const LayerSpec& L) {
+  static const int pp_on = getenv("HB_PP") ? atoi(getenv("HB_PP")) : 1;
+  return (pp_on && pp_eligible(L)) ? KIND_PP : KIND_TC;
+}
+// Input layout (phases Q) a conv of `kind` reads: K4 reads I (s=1) / S (s=2).
+int layer_in_q(const LayerSpec& L, int kind) { return kind == KIND_PP ? L.stride * pp_phases(L.cout) : L.stride; }
+size_t layer_wbytes(const LayerSpec& L, int kind) {
+  return kind == KIND_PP ? pp_wbytes(L.cin, L.cout, L.stride) : wpack_bytes(L.cin, L.cout);
+}
+void layer_pack(const LayerSpec& L, int kind, const float* w, uint16_t* dst) {
+  if (kind == KIND_PP) pp_pack_weights(w, L.cin, L.cout, L.stride, dst);
+  else pack_weights(w, L.cin, L.cout, L.stride, dst);
+}
+// Rows per activation plane that hold any Q-phase layout (Q <= 32) of length L.
+int plane_rows_max(int L) { return round_up(L, 256); }
+
+struct LayerPlan {
+  int kind = KIND_TC;
+  ConvPlan tc;
+  PPPlan pp;
+};
+cudaError_t launch_layer(const LayerPlan& lp, cudaStream_t st) {
+  return lp.kind == KIND_PP ? launch_pp(lp.pp, st) : launch_conv(lp.tc, st);
+}
+
 struct Group {
   int width = 0, depth = 0, lead_any = 0, lane = 0;
   std::vector<int> mi;                 // positions in hb_ctx::selected (zoo order)
   std::vector<LayerSpec> layers;
+  std::vector<int> kind;               // per layer (index 0 = stem, unused)
   std::vector<std::vector<StemMember>> stem;  // [chunk][member]: its lead's windows (chunk rows), stem weights
   std::vector<uint8_t*> wpack;         // per conv layer: [G][member image]
   std::vector<float*> bias;            // per conv layer: [G][bias_len]
@@ -65,6 +100,7 @@ struct Group {
 struct Member {
   int idx = -1, lead = 0, width = 0, depth = 0;
   std::vector<LayerSpec> layers;
+  std::vector<uint8_t*> wpp;    // per conv layer: K4b weight image (null if not eligible)
   float* stem_w = nullptr;  // [w][16]
   float* stem_b = nullptr;
   std::vector<uint8_t*> wpack;  // per conv layer (layers[1..])
@@ -110,7 +146,7 @@ struct hb_ctx {
   float* ens_prob = nullptr;
   float* ens_logit = nullptr;
   float* ens_sums = nullptr;  // [2][P]: sum of member sigmoids, sum of member logits
-  std::vector<ConvPlan> plans;
+  std::vector<LayerPlan> plans;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
   bool timed = false;
@@ -166,6 +202,7 @@ void free_member(Member& m) {
   cudaFree(m.stem_w);
   cudaFree(m.stem_b);
   for (auto p : m.wpack) cudaFree(p);
+  for (auto p : m.wpp) cudaFree(p);
   for (auto p : m.bias) cudaFree(p);
   cudaFree(m.fc_w);
 }
@@ -221,13 +258,13 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
     const double rows = static_cast<double>(c->Pc) * G;
     const LayerSpec& s0 = g.layers[0];
     for (int ch = 0; ch < c->n_chunks; ++ch) {
-      CK(c, launch_stem(g.stem[ch].data(), G, c->W, c->Pc, c->W, round_up(s0.lout, 8), s0.cout, s0.pad,
-                        c->act[3 * ln], ms));
+      CK(c, launch_stem(g.stem[ch].data(), G, c->W, c->Pc, c->W, layer_in_q(g.layers[1], g.kind[1]), s0.cout,
+                        s0.pad, c->act[3 * ln], ms));
       pr->mark(ms, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
       size_t pi = g.plan0[ch];
       for (size_t li = 1; li < g.layers.size(); ++li) {
         const LayerSpec& L = g.layers[li];
-        CK(c, launch_conv(c->plans[pi++], ms));
+        CK(c, launch_layer(c->plans[pi++], ms));
         pr->mark(ms, K_CONV, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
                  rows * 2.0 * (static_cast<double>(L.cin) * L.lin +
                                (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
@@ -268,6 +305,7 @@ int build_selection(hb_ctx* c) {
       gp->width = m.width;
       gp->depth = m.depth;
       gp->layers = m.layers;
+      gp->kind.assign(gp->layers.size(), KIND_TC);
     }
     gp->mi.push_back(mi);
     gp->flops += m.flops;
@@ -293,7 +331,7 @@ int build_selection(hb_ctx* c) {
     for (auto& g : c->groups)
       for (auto& L : g.layers)
         need[g.lane] = std::max(need[g.lane], static_cast<size_t>(pc) * g.mi.size() * L.cout *
-                                                  act_rows(L.lout, 1) * sizeof(__half));
+                                                  plane_rows_max(L.lout) * sizeof(__half));
     double tot = 0;
     for (size_t v : need) tot += 3.0 * v;
     return tot;
@@ -327,17 +365,19 @@ int build_selection(hb_ctx* c) {
   for (auto& g : c->groups) {
     const int G = static_cast<int>(g.mi.size());
     const int c_last = g.layers.back().cout;
+    for (size_t li = 1; li < g.layers.size(); ++li) g.kind[li] = layer_kind(g.layers[li]);
     // group-contiguous weight images (device-to-device from the registered members)
     for (size_t li = 1; li < g.layers.size(); ++li) {
       const LayerSpec& L = g.layers[li];
-      const size_t wb = wpack_bytes(L.cin, L.cout), bl = bias_len(L.cout);
+      const size_t wb = layer_wbytes(L, g.kind[li]), bl = bias_len(L.cout);
       uint8_t* w;
       float* b;
       CK(c, cudaMalloc(&w, wb * G));
       CK(c, cudaMalloc(&b, sizeof(float) * bl * G));
       for (int k = 0; k < G; ++k) {
         const Member& m = c->members[c->selected[g.mi[k]]];
-        CK(c, cudaMemcpy(w + wb * k, m.wpack[li - 1], wb, cudaMemcpyDeviceToDevice));
+        CK(c, cudaMemcpy(w + wb * k, g.kind[li] == KIND_PP ? m.wpp[li - 1] : m.wpack[li - 1], wb,
+                         cudaMemcpyDeviceToDevice));
         CK(c, cudaMemcpy(b + bl * k, m.bias[li - 1], sizeof(float) * bl, cudaMemcpyDeviceToDevice));
       }
       g.wpack.push_back(w);
@@ -365,33 +405,41 @@ int build_selection(hb_ctx* c) {
     for (int ch = 0; ch < c->n_chunks; ++ch) {
       g.plan0.push_back(c->plans.size());
       int cur = 0;
-      const int nblocks = static_cast<int>(g.layers.size() - 1) / 2;
+      auto in_q = [&](size_t li) { return layer_in_q(g.layers[li], g.kind[li]); };
       for (size_t li = 1; li < g.layers.size(); ++li) {
         const LayerSpec& L = g.layers[li];
         const bool conv1 = (li % 2 == 1);
-        const int blk = static_cast<int>(li - 1) / 2;
-        int src = cur, dst, out_split = 0, res_len = 0;
+        int src = cur, dst, out_q = 1, res_len = 0, res_q = 1;
         const __half* res = nullptr;
         if (conv1) {
           dst = (cur + 1) % 3;
+          out_q = in_q(li + 1);  // h feeds conv2
         } else {
           src = (cur + 1) % 3;
           dst = (cur + 2) % 3;
           res = act[cur];
           res_len = g.layers[li - 1].lin;
-          // the output of an even block feeds the next (stride-2) block: parity-split layout
-          out_split = (blk % 2 == 0 && blk + 1 < nblocks) ? 1 : 0;
+          res_q = in_q(li - 1);  // the block input, as conv1 read it
+          // the block output feeds the next block's conv1 in the layout that conv reads
+          out_q = (li + 1 < g.layers.size()) ? in_q(li + 1) : 1;
         }
-        ConvPlan plan;
         // head partials of chunk ch: rows [ch*Pc, (ch+1)*Pc) of every member's [P_pad][head_mt] block
         float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
-        const char* e = plan_conv(&plan, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
-                                  L.head ? nullptr : act[dst], out_split, g.wpack[li - 1], g.bias[li - 1], res,
-                                  conv1 ? 0 : L.res_mode, L.res_c, res_len, L.head ? g.fc_w : nullptr, head_base,
-                                  c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
+        LayerPlan plan;
+        plan.kind = g.kind[li];
+        const char* e;
+        if (plan.kind == KIND_PP) {
+          e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src], act[dst], out_q,
+                      g.wpack[li - 1], g.bias[li - 1], res, conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q,
+                      c->num_sms);
+        } else {
+          e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+                        L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
+                        conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, L.head ? g.fc_w : nullptr, head_base,
+                        c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
+          if (!e && L.head && plan.tc.args.n_ntiles * plan.tc.args.mt_per_p != g.head_mt) e = "head tiling mismatch";
+        }
         if (e) return fail(c, HB_E_INVALID, e);
-        if (L.head && plan.args.n_ntiles * plan.args.mt_per_p != g.head_mt)
-          return fail(c, HB_E_INVALID, "head tiling mismatch");
         c->plans.push_back(plan);
         if (!conv1) cur = dst;
       }
@@ -524,13 +572,20 @@ int hb_add_member(hb_ctx* c, int idx, int lead, int width, int depth, const floa
   p += s0.cout;
   for (size_t li = 1; li < m.layers.size(); ++li) {
     const LayerSpec& L = m.layers[li];
-    const size_t wb = wpack_bytes(L.cin, L.cout);
-    std::vector<uint16_t> img(wb / 2);
-    pack_weights(p, L.cin, L.cout, L.stride, img.data());
-    uint8_t* dw;
-    CK(c, cudaMalloc(&dw, wb));
-    CK(c, cudaMemcpy(dw, img.data(), wb, cudaMemcpyHostToDevice));
-    m.wpack.push_back(dw);
+    // both weight images: the kernel per layer is chosen when the selection is built
+    for (int kind = KIND_TC; kind <= KIND_PP; ++kind) {
+      if (kind == KIND_PP && !pp_eligible(L)) {
+        m.wpp.push_back(nullptr);
+        continue;
+      }
+      const size_t wb = layer_wbytes(L, kind);
+      std::vector<uint16_t> img(wb / 2);
+      layer_pack(L, kind, p, img.data());
+      uint8_t* dw;
+      CK(c, cudaMalloc(&dw, wb));
+      CK(c, cudaMemcpy(dw, img.data(), wb, cudaMemcpyHostToDevice));
+      (kind == KIND_PP ? m.wpp : m.wpack).push_back(dw);
+    }
     p += static_cast<size_t>(L.cout) * L.cin * kTaps;
     const int bn = conv_bn(L.cout);
     const int nbias = ((round_up(L.cout, 16) + bn - 1) / bn) * bn;
@@ -770,9 +825,9 @@ int hb_tick_work(const hb_ctx* c, double* flops, double* bytes) {
 
 // ----------------------------------------------------------------- test entry points
 
-int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
-                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
-                 const float* fc_w_host, float* head_out, void* stream) {
+int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
+                   int cout, const void* res, int res_mode, int res_c, int res_len, int res_q, void* out, int out_q,
+                   const float* fc_w_host, float* head_out, int kind, void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
@@ -782,11 +837,13 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
   const int lout = (lin + stride - 1) / stride;
   const int tot = (lout - 1) * stride + kTaps - lin;
   const int pad = tot > 0 ? tot / 2 : 0;
-  const size_t wb = wpack_bytes(cin, cout);
+  if (kind < 0) kind = layer_kind({cin, cout, stride, lin, lout, pad, res_mode, res_c, fc_w_host ? 1 : 0});
+  if (kind == KIND_PP && fc_w_host) return fail(nullptr, HB_E_INVALID, "conv_pp: no fused head");
+  const LayerSpec spec{cin, cout, stride, lin, lout, pad, res_mode, res_c, fc_w_host ? 1 : 0};
+  const size_t wb = layer_wbytes(spec, kind);
   std::vector<uint16_t> img(wb / 2);
-  pack_weights(w_host, cin, cout, stride, img.data());
-  const int bn = conv_bn(cout);
-  const int nbias = ((round_up(cout, 16) + bn - 1) / bn) * bn;
+  layer_pack(spec, kind, w_host, img.data());
+  const int nbias = static_cast<int>(bias_len(cout));
   std::vector<float> bias(nbias, 0.f);
   std::copy(b_host, b_host + cout, bias.begin());
   uint8_t* dw = nullptr;
@@ -800,16 +857,23 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
     CK(none, cudaMalloc(&dfc, sizeof(float) * cout));
     CK(none, cudaMemcpy(dfc, fc_w_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
   }
-  ConvPlan plan;
-  const char* e = plan_conv(&plan, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
-                            static_cast<__half*>(out), out_split, dw, db, static_cast<const __half*>(res), res_mode,
-                            res_c, res_len > 0 ? res_len : lout, dfc, head_out, sms);
+  LayerPlan plan;
+  plan.kind = kind;
+  const char* e;
+  if (kind == KIND_PP)
+    e = plan_pp(&plan.pp, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
+                static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
+                res_len > 0 ? res_len : lout, res_q, sms);
+  else
+    e = plan_conv(&plan.tc, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
+                  static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
+                  res_len > 0 ? res_len : lout, res_q, dfc, head_out, sms);
   int rc = HB_OK;
   if (e) {
     g_create_err = e;
     rc = HB_E_INVALID;
   } else {
-    cudaError_t ce = launch_conv(plan, st);
+    cudaError_t ce = launch_layer(plan, st);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) {
       g_create_err = std::string("conv launch: ") + cudaGetErrorString(ce);
@@ -822,6 +886,17 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
   return rc;
 }
 
+int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const float* w_host, const float* b_host,
+                 int cout, const void* res, int res_mode, int res_c, int res_len, void* out, int out_split,
+                 const float* fc_w_host, float* head_out, void* stream) {
+  return hb_op_conv1d_q(in, P, cin, lin, stride, w_host, b_host, cout, res, res_mode, res_c, res_len,
+                        res_mode == 2 ? 2 : 1, out, out_split ? 2 : 1, fc_w_host, head_out, KIND_TC, stream);
+}
+
+int hb_conv_kind(int cin, int cout, int stride, int head) {
+  return layer_kind({cin, cout, stride, 0, 0, 0, 0, 0, head});
+}
+
 int hb_conv_mt(int cin, int cout, int lin, int stride, int head) {
   const int lout = (lin + stride - 1) / stride;
   const int rows = head ? lout : act_rows(lout, 0);
@@ -830,7 +905,7 @@ int hb_conv_mt(int cin, int cout, int lin, int stride, int head) {
   return (head ? nnt : 1) * ((rows + sm - 1) / sm);
 }
 
-int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out) {
+int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode, int kind, int iters, float* ms_out) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
@@ -839,9 +914,11 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
   const int lout = (lin + stride - 1) / stride;
   const int tot = (lout - 1) * stride + kTaps - lin;
   const int pad = tot > 0 ? tot / 2 : 0;
-  const size_t in_b = static_cast<size_t>(P) * cin * act_rows(lin, 1) * 2;
-  const size_t out_b = static_cast<size_t>(P) * cout * act_rows(lout, 1) * 2;
-  const size_t wb = wpack_bytes(cin, cout);
+  const size_t in_b = static_cast<size_t>(P) * cin * plane_rows_max(lin) * 2;
+  const size_t out_b = static_cast<size_t>(P) * cout * plane_rows_max(lout) * 2;
+  if (kind < 0) kind = layer_kind({cin, cout, stride, lin, lout, pad, res_mode, cin < cout ? cin : cout, 0});
+  const LayerSpec spec{cin, cout, stride, lin, lout, pad, res_mode, cin < cout ? cin : cout, 0};
+  const size_t wb = layer_wbytes(spec, kind);
   const int bn = conv_bn(cout);
   const int nbias = ((round_up(cout, 16) + bn - 1) / bn) * bn;
   void *din = nullptr, *dout = nullptr, *dres = nullptr, *dw = nullptr, *db = nullptr;
@@ -855,17 +932,28 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
   CK(none, cudaMemset(dw, 0, wb));
   CK(none, cudaMalloc(&db, nbias * 4));
   CK(none, cudaMemset(db, 0, nbias * 4));
-  ConvPlan plan;
-  const char* e = plan_conv(&plan, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
-                            static_cast<__half*>(dout), 0, static_cast<uint8_t*>(dw), static_cast<float*>(db),
-                            res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
-                            res_mode == 2 ? 2 * lin : lout, nullptr, nullptr, sms);
+  LayerPlan plan;
+  plan.kind = kind;
+  const int in_q = layer_in_q(spec, kind);
+  const int out_q = kind == KIND_PP ? pp_phases(cout) : 1;  // as if feeding a like layer
+  const int res_q = res_mode == 2 ? in_q : out_q;
+  const char* e;
+  if (kind == KIND_PP)
+    e = plan_pp(&plan.pp, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
+                static_cast<__half*>(dout), out_q, static_cast<uint8_t*>(dw), static_cast<float*>(db),
+                res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
+                res_mode == 2 ? 2 * lin : lout, res_q, sms);
+  else
+    e = plan_conv(&plan.tc, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
+                  static_cast<__half*>(dout), out_q, static_cast<uint8_t*>(dw), static_cast<float*>(db),
+                  res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
+                  res_mode == 2 ? 2 * lin : lout, res_q, nullptr, nullptr, sms);
   int rc = HB_OK;
   unsigned long long* dprof = nullptr;
-  if (!e && (plan.args.dbg & 8)) {
-    cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * plan.grid);
-    cudaMemset(dprof, 0, sizeof(unsigned long long) * 8 * plan.grid);
-    plan.args.prof = dprof;
+  if (!e && kind == KIND_TC && (plan.tc.args.dbg & 8)) {
+    cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * plan.tc.grid);
+    cudaMemset(dprof, 0, sizeof(unsigned long long) * 8 * plan.tc.grid);
+    plan.tc.args.prof = dprof;
   }
   if (e) {
     g_create_err = e;
@@ -876,9 +964,9 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int i = 0; i < 3; ++i) launch_conv(plan, st);
+    for (int i = 0; i < 3; ++i) launch_layer(plan, st);
     cudaEventRecord(a, st);
-    for (int i = 0; i < iters; ++i) launch_conv(plan, st);
+    for (int i = 0; i < iters; ++i) launch_layer(plan, st);
     cudaEventRecord(b, st);
     cudaError_t ce = cudaStreamSynchronize(st);
     float ms = 0.f;
@@ -888,12 +976,12 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
     cudaEventDestroy(b);
     cudaStreamDestroy(st);
     if (dprof) {
-      std::vector<unsigned long long> h(8 * plan.grid);
+      std::vector<unsigned long long> h(8 * plan.tc.grid);
       cudaMemcpy(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost);
       double sum[8] = {0};
-      for (int i = 0; i < plan.grid; ++i)
-        for (int k = 0; k < 8; ++k) sum[k] += static_cast<double>(h[i * 8 + k]) / plan.grid;
-      const double tiles = static_cast<double>(plan.args.num_tiles) / plan.grid;
+      for (int i = 0; i < plan.tc.grid; ++i)
+        for (int k = 0; k < 8; ++k) sum[k] += static_cast<double>(h[i * 8 + k]) / plan.tc.grid;
+      const double tiles = static_cast<double>(plan.tc.args.num_tiles) / plan.tc.grid;
       fprintf(stderr, "[prof] per tile (cycles): mma wait_acc %.0f wait_a %.0f issue %.0f | epi wait %.0f work %.0f | epi total/tile %.0f (tiles/CTA %.1f)\n",
               sum[0] / tiles, sum[1] / tiles, sum[2] / tiles, sum[3] / tiles, sum[4] / tiles, sum[5] / tiles, tiles);
       cudaFree(dprof);
@@ -911,8 +999,12 @@ int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, i
   return rc;
 }
 
-int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
-               void* stream) {
+int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out) {
+  return hb_bench_conv_k(P, cin, cout, lin, stride, res_mode, KIND_TC, iters, ms_out);
+}
+
+int hb_op_stem_q(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
+                 int out_q, void* stream) {
   if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int tot = kTaps - 1;
@@ -923,12 +1015,17 @@ int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b
   CK(none, cudaMalloc(&db, sizeof(float) * cout));
   CK(none, cudaMemcpy(db, b_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
   const StemMember sm{static_cast<const __half*>(xn), dw, db};
-  cudaError_t ce = launch_stem(&sm, 1, L, P, L, round_up(L, 8), cout, tot / 2, static_cast<__half*>(out), st);
+  cudaError_t ce = launch_stem(&sm, 1, L, P, L, out_q, cout, tot / 2, static_cast<__half*>(out), st);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
   cudaFree(dw);
   cudaFree(db);
   if (ce != cudaSuccess) return fail(none, HB_E_CUDA, cudaGetErrorString(ce));
   return HB_OK;
+}
+
+int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
+               void* stream) {
+  return hb_op_stem_q(xn, P, L, w_host, b_host, cout, out, 1, stream);
 }
 
 }  // extern "C"

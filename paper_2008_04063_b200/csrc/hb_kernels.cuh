@@ -31,13 +31,30 @@ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 inline int lp_I(int L) { return round_up(L, 8); }
 inline int lh_S(int L) { return round_up((L + 1) / 2, 8); }
 inline int act_rows(int L, int split) { return split ? 2 * lh_S(L) : lp_I(L); }
+// General Q-phase layout (Q a power of two; I = Q1, S = Q2): per plane, Q
+// phase sub-planes of lq_Q(L, Q) rows; position l at phase l % Q, row l / Q:
+//   element (((p*G+g)*Q + l%Q)*lq + l/Q)*8 + c
+// The polyphase conv (conv_pp.cu) reads its input with Q = stride * 128/cout.
+// Q * lq_Q(L, Q) is the smallest multiple of 8Q >= L, so every Q <= 32 fits in
+// roundup(L, 256) rows per plane.
+inline int lq_Q(int L, int Q) { return round_up((L + Q - 1) / Q, 8); }
+inline int act_rows_q(int L, int Q) { return Q * lq_Q(L, Q); }
+inline int ilog2(int q) {
+  int s = 0;
+  while ((1 << s) < q) ++s;
+  return s;
+}
+__host__ __device__ __forceinline__ size_t q_off(size_t plane, int qs, int lq, int l) {
+  return (((plane << qs) + static_cast<size_t>(l & ((1 << qs) - 1))) * static_cast<size_t>(lq) +
+          static_cast<size_t>(l >> qs)) * 8;
+}
 
 struct ConvArgs {
   int P, cin, cout, bn, n_ntiles;  // P = G*Pm rows of the activation tensors; bn = per-tile N (mult of 16, <=256)
   int G, Pm;                       // members sharing this layer shape (one launch), patients per member
   int fold, bnp, stride_m;         // taps folded into N (D' = [128 x fold*bn]), MMA N, output rows per M tile
   int lin, lout;
-  int out_split, out_lp, out_lh;   // output layout (I: out_lp rows; S: 2 x out_lh rows)
+  int out_qs, out_lq;              // output layout: Q = 1 << out_qs phases of out_lq rows
   int out_rows;                    // positions that must be written (valid or zero padding)
   int stride, pad, row0;           // row0: first A row (s=1) / pair (s=2) loaded, multiple of 8
   int ck, n_kchunks, rows;         // channels per k-chunk, A rows per (parity, group) region
@@ -50,10 +67,10 @@ struct ConvArgs {
   const float* bias;               // [G][n_ntiles*bn] (zero padded)
   int bias_stride;                 // floats per member
   int sb_len;                      // floats of bias (and of fc) cached in smem: G*bn, 0 = read global
-  __half* out;                     // output activation (layout out_split)
+  __half* out;                     // output activation (Q-phase layout out_qs)
   const __half* res;               // shortcut source or null
-  int res_mode;                    // 0 none, 1 identity (I layout), 2 maxpool(2) (S layout)
-  int res_c, res_rows;             // shortcut channels; plane rows (I: lp, S: lh)
+  int res_mode;                    // 0 none, 1 identity, 2 maxpool(2)
+  int res_c, res_qs, res_lq;       // shortcut channels; its layout (1 << res_qs phases of res_lq rows)
   int relu;
   const float* fc_w;               // head: [G][cout] -> head_out[G*Pm][n_ntiles][mt_per_p] (null = no head)
   float* head_out;
@@ -69,14 +86,53 @@ struct ConvPlan {
   uint32_t smem_bytes;
 };
 
+// K4b polyphase conv (conv_pp.cu): narrow layers, M = (output phase, C_out).
+struct PPArgs {
+  int G, Pm, P;                    // members of one launch, patients per member, P = G*Pm
+  int cin, cout, stride, pad, lin, lout;
+  int ph, Q, qs, U;                // output phases 128/cout, input phases stride*ph = 1 << qs, shifts
+  int n_pairs;                     // 16-channel K groups (cin / 16)
+  uint32_t w_par16;                // one tap-parity array, 16-B units
+  uint32_t w_half_bytes, w_pair_bytes, w_bytes;  // weight image: [pair][half][parity][entry][cout][16 B]
+  size_t w_stride;                 // bytes per member image
+  int in_lq;                       // input rows per phase plane
+  int nb, R;                       // MMA N (columns per tile); rows per phase plane in a B stage
+  uint32_t stage_bytes;            // 2 halves x Q phases x R rows x 16 B
+  int n_stages;
+  int nt_per_p, num_tiles;
+  uint32_t tmem_cols;
+  const uint8_t* wimg;
+  const float* bias;
+  int bias_stride;
+  __half* out;
+  int out_qs, out_lq, out_rows;
+  const __half* res;
+  int res_mode, res_c, res_qs, res_lq;
+};
+struct PPPlan {
+  PPArgs args;
+  CUtensorMap tmap;                // input view {8-row lines, lines, Q phases, planes}
+  int grid;
+  uint32_t smem_bytes;
+};
+bool pp_shape_ok(int cin, int cout, int stride);
+int pp_phases(int cout);           // 128 / cout; the input of a pp conv is in Q = stride * phases layout
+size_t pp_wbytes(int cin, int cout, int stride);
+void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */);
+const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
+                    const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms);
+cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
+cudaError_t init_pp_kernel();
+
 // Build a plan (tensor map + tiling) for one conv layer.  The input layout is
-// I for stride 1 and S for stride 2; res (if any) is I for identity, S for
-// maxpool; `out_split` selects the output layout.  Returns 0 or an error string.
+// I for stride 1 and S for stride 2; res (if any) and the output may use any
+// Q-phase layout (res_q, out_q).  Returns 0 or an error string.
 // G members of identical layer shape run in one launch: activations are
 // [G*Pm] patients deep, weights / bias / fc are G consecutive per-member images.
 const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
-                      const __half* in, __half* out, int out_split, const uint8_t* wpack, const float* bias,
-                      const __half* res, int res_mode, int res_c, int res_len, const float* fc_w,
+                      const __half* in, __half* out, int out_q, const uint8_t* wpack, const float* bias,
+                      const __half* res, int res_mode, int res_c, int res_len, int res_q, const float* fc_w,
                       float* head_out, int num_sms, size_t head_g_stride = 0);
 size_t bias_len(int cout);  // per-member bias floats (zero padded to whole N tiles)
 int conv_fold(int cin, int cout, int stride);  // taps folded into the MMA N dimension (1, 2 or 4)
@@ -109,6 +165,7 @@ cudaError_t init_stream_kernels();
 cudaError_t init_stem_kernel();
 inline cudaError_t init_kernels() {
   cudaError_t e = init_conv_kernel();
+  if (e == cudaSuccess) e = init_pp_kernel();
   return e != cudaSuccess ? e : init_stream_kernels();
 }
 
@@ -122,7 +179,7 @@ struct StemMember {
 };
 constexpr int kMaxGroup = 16;
 cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int G, int x_stride, int Pm, int L,
-                        int lp_out, int cout, int pad, __half* out, cudaStream_t st);
+                        int out_q, int cout, int pad, __half* out, cudaStream_t st);  // out: Q-phase layout
 
 // K1+K2: ring append of `n_new` samples per stream at the device write cursor
 // *wpos, then (if xn != null) gather of the window ending at *wpos + n_new and

@@ -23,7 +23,7 @@ constexpr int kStemSmemCap = 48 * 1024;  // largest dynamic-smem pad (4 CTAs/SM 
 
 struct StemTcArgs {
   StemMember m[kMaxGroup];
-  int G, Pm, x_stride, L, lp_out, cout, n_mma, pad, mt_per_row, num_tiles;
+  int G, Pm, x_stride, L, out_qs, out_lq, out_rows, cout, n_mma, pad, mt_per_row, num_tiles;
   __half* out;
 };
 
@@ -113,9 +113,8 @@ __global__ void __launch_bounds__(kStemTcThreads) stem_tc_kernel(const __grid_co
     phase ^= 1;
     tc_fence_after();
     const int l = l0 + r;
-    const bool in_buf = l < a.lp_out, valid = l < a.L;
+    const bool in_buf = l < a.out_rows, valid = l < a.L;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    __half* orow = a.out + static_cast<size_t>(row) * (a.cout / 8) * a.lp_out * 8;
     for (int c16 = 0; c16 * 16 < a.cout; ++c16) {  // warp-collective loads: every lane takes part
       float v[16];
       tmem_ld16(taddr + static_cast<uint32_t>(c16 * 16), v);
@@ -131,7 +130,7 @@ __global__ void __launch_bounds__(kStemTcThreads) stem_tc_kernel(const __grid_co
           const float y1 = fmaxf(v[8 * h + k + 1] + sbias[g8 * 8 + k + 1], 0.f);
           o2[k / 2] = valid ? __floats2half2_rn(y0, y1) : __floats2half2_rn(0.f, 0.f);
         }
-        *reinterpret_cast<uint4*>(orow + (static_cast<size_t>(g8) * a.lp_out + l) * 8) = pk;
+        *reinterpret_cast<uint4*>(a.out + q_off(static_cast<size_t>(row) * (a.cout / 8) + g8, a.out_qs, a.out_lq, l)) = pk;
       }
     }
     tc_fence_before();
@@ -147,7 +146,7 @@ cudaError_t init_stem_kernel() {
   return cudaFuncSetAttribute(stem_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStemSmemCap);
 }
 
-cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int lp_out, int cout, int pad,
+cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
                         __half* out, cudaStream_t st) {
   if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup) return cudaErrorInvalidValue;
   StemTcArgs a;
@@ -156,11 +155,13 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
   a.Pm = Pm;
   a.x_stride = x_stride;
   a.L = L;
-  a.lp_out = lp_out;
+  a.out_qs = ilog2(out_q);
+  a.out_lq = lq_Q(L, out_q);
+  a.out_rows = act_rows_q(L, out_q);
   a.cout = cout;
   a.n_mma = cout < 16 ? 16 : cout;  // M=128 needs N >= 16
   a.pad = pad;
-  a.mt_per_row = (lp_out + kBM - 1) / kBM;
+  a.mt_per_row = (a.out_rows + kBM - 1) / kBM;
   a.num_tiles = G * Pm * a.mt_per_row;
   a.out = out;
   int dev = 0, sms = 148;

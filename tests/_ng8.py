@@ -41,3 +41,37 @@ def from_split(a: torch.Tensor, C: int, L: int) -> torch.Tensor:
     g[:, :, 0::2, :] = a[:, :, 0, : (L + 1) // 2, :]
     g[:, :, 1::2, :] = a[:, :, 1, : L // 2, :]
     return g.permute(0, 1, 3, 2).reshape(P, C, L)
+
+
+def lq(length: int, q: int) -> int:
+    return (-(-length // q) + 7) // 8 * 8
+
+
+def to_q(x: torch.Tensor, q: int) -> torch.Tensor:
+    """[P, C, L] -> Q-phase layout [P, C/8, Q, lq, 8] fp16 (position l at phase l % Q, row l // Q), zero padded."""
+    P, C, L = x.shape
+    rows = lq(L, q)
+    out = torch.zeros(P, C // 8, q, rows, 8, dtype=torch.float16, device=x.device)
+    g = x.reshape(P, C // 8, 8, L).permute(0, 1, 3, 2).to(torch.float16)  # [P, G, L, 8]
+    for ph in range(q):
+        n = len(range(ph, L, q))
+        out[:, :, ph, :n, :] = g[:, :, ph::q, :]
+    return out.contiguous()
+
+
+def from_q(a: torch.Tensor, C: int, L: int, q: int) -> torch.Tensor:
+    P = a.shape[0]
+    g = torch.empty(P, C // 8, L, 8, dtype=a.dtype, device=a.device)
+    for ph in range(q):
+        n = len(range(ph, L, q))
+        g[:, :, ph::q, :] = a[:, :, ph, :n, :]
+    return g.permute(0, 1, 3, 2).reshape(P, C, L)
+
+
+def q_padding_zero(a: torch.Tensor, L: int, q: int) -> bool:
+    """Every slot of the Q-phase planes past position L holds zero."""
+    for ph in range(q):
+        n = len(range(ph, L, q))
+        if not bool((a[:, :, ph, n:, :] == 0).all()):
+            return False
+    return True
