@@ -34,9 +34,9 @@
 //    plane.  One TMA box per (tile, 16-channel pair) brings every phase of
 //    the tile's row range; shift u is a descriptor offset.
 //
-// Roles (384 threads, 1 CTA/SM, persistent over tiles) as in K4: warp 0 TMA
-// producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 / 8-11 two
-// epilogue warpgroups (one per TMEM accumulator).  Epilogue thread r holds M
+// Roles (640 threads, 1 CTA/SM, persistent over tiles): warp 0 TMA producer,
+// warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-19 four epilogue
+// warpgroups (two per TMEM accumulator, one per half of its columns).  Epilogue thread r holds M
 // row r = (p', c) for nb columns; an 8x8 register transpose by warp shuffles
 // inside each 8-lane group turns that into 8 channels x one position per
 // lane, so the shortcut read and the output store are 16-byte rows.
@@ -48,6 +48,8 @@
 #include <cstring>
 
 namespace hb {
+
+constexpr int kPPThreads = 640;  // warp 0 TMA, 1 MMA, 2 TMEM, 4-19 four epilogue warpgroups
 
 struct PPTile {
   int g, p, nt;  // member of the group, global patient row [G*Pm], column tile
@@ -63,23 +65,44 @@ __device__ __forceinline__ PPTile pp_tile(const PPArgs& a, int tile) {
   return t;
 }
 
-// 8x8 transpose inside aligned 8-lane groups: lane r8 holds row r8 (its
-// channel) at 8 columns; afterwards it holds column r8 across the 8 channels.
-__device__ __forceinline__ void transpose8(float (&v)[8], int r8) {
+// 8x8 transpose of fp16 values inside aligned 8-lane groups: lane r8 holds
+// row r8 (its channel) as 4 half2 registers
+// (columns 2k, 2k+1); afterwards it holds column r8 (channels 2k, 2k+1 in
+// register k).  Two register exchanges per 4x4 / 2x2 stage; the single-
+// element stage moves two halves per shuffle (byte permutes): 6 shuffles per
+// 8x8 block (an fp32 transpose takes 12 shuffles + 24 selects).
+__device__ __forceinline__ void transpose8_h2(uint32_t (&h)[4], int r8) {
+  {
+    const bool hi = (r8 & 4) != 0;
 #pragma unroll
-  for (int m = 4; m >= 1; m >>= 1) {
-    const bool hi = (r8 & m) != 0;
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, hi ? h[k] : h[k + 2], 4);
+      if (hi) h[k] = recv; else h[k + 2] = recv;
+    }
+  }
+  {
+    const bool hi = (r8 & 2) != 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k & m) continue;
-      const float send = hi ? v[k] : v[k | m];
-      const float recv = __shfl_xor_sync(0xffffffffu, send, m);
-      if (hi) v[k] = recv; else v[k | m] = recv;
+    for (int k = 0; k < 4; k += 2) {
+      const uint32_t recv = __shfl_xor_sync(0xffffffffu, hi ? h[k] : h[k + 1], 2);
+      if (hi) h[k] = recv; else h[k + 1] = recv;
+    }
+  }
+  {
+    const bool hi = (r8 & 1) != 0;
+    const uint32_t s_send = hi ? 0x5410u : 0x7632u;
+    const uint32_t s_a = hi ? 0x3254u : 0x5410u;
+    const uint32_t s_b = hi ? 0x3276u : 0x7610u;
+#pragma unroll
+    for (int k = 0; k < 4; k += 2) {
+      const uint32_t r = __shfl_xor_sync(0xffffffffu, __byte_perm(h[k], h[k + 1], s_send), 1);
+      h[k] = __byte_perm(h[k], r, s_a);
+      h[k + 1] = __byte_perm(h[k + 1], r, s_b);
     }
   }
 }
 
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kPPThreads, 1)
     conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ PPArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
@@ -105,7 +128,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     mbar_init(w_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], 256);  // two epilogue warpgroups per buffer
     }
     fence_barrier_init();
   }
@@ -150,12 +173,35 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
         for (int j = 0; j < a.n_pairs; ++j) {
           mbar_wait(&st_empty[st], sph ^ 1u, 102);
-          mbar_arrive_expect_tx(&st_full[st], a.stage_bytes);
-          tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmB, &st_full[st], 0, line0, 0,
-                      t.p * planes_per_p + 2 * j);
+          if (a.dbg & 4) {
+            mbar_arrive(&st_full[st]);
+          } else {
+            mbar_arrive_expect_tx(&st_full[st], a.stage_bytes);
+            tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmB, &st_full[st], 0, line0, 0,
+                        t.p * planes_per_p + 2 * j);
+          }
           if (++st == a.n_stages) {
             st = 0;
             sph ^= 1u;
+          }
+        }
+        // The epilogue's shortcut reads are plain loads with little in
+        // flight; pull this tile's shortcut rows into L2 now (the tile is
+        // ~2 tiles ahead of its epilogue) so they hit L2.
+        if (a.res_mode && !(a.dbg & 8)) {
+          const int sc = a.res_mode == 2 ? 2 : 1;
+          const int pos_lo = sc * a.ph * t.nt * a.nb;
+          int pos_hi = sc * a.ph * (t.nt + 1) * a.nb;
+          const int res_rows = (1 << a.res_qs) * a.res_lq;
+          if (pos_hi > res_rows) pos_hi = res_rows;
+          const int r_lo = pos_lo >> a.res_qs, r_hi = min(a.res_lq, ((pos_hi - 1) >> a.res_qs) + 1);
+          if (r_hi > r_lo) {
+            const uint32_t bytes = static_cast<uint32_t>(r_hi - r_lo) * 16u;
+            for (int g = 0; g < a.res_c / 8; ++g)
+              for (int q = 0; q < (1 << a.res_qs); ++q) {
+                const size_t plane = static_cast<size_t>(t.p) * (a.res_c / 8) + g;
+                bulk_prefetch_l2(a.res + (((plane << a.res_qs) + q) * a.res_lq + r_lo) * 8, bytes);
+              }
           }
         }
       }
@@ -170,6 +216,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint32_t accph = 0;
     uint32_t wph = 0;
     int cur_g = static_cast<int>(blockIdx.x) < a.num_tiles ? pp_tile(a, blockIdx.x).g : 0;
+    const bool prof = (a.dbg & 16) && a.prof && lane == 0;
+    unsigned long long c_acc = 0, c_b = 0, c_start = prof ? clock64() : 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const PPTile t = pp_tile(a, tile);
       if (t.g != cur_g) {
@@ -177,11 +225,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         cur_g = t.g;
       }
       mbar_wait(w_full, wph, 111);
+      unsigned long long t0 = prof ? clock64() : 0;
       mbar_wait(&acc_empty[acc], accph ^ 1u, 112);
+      if (prof) {
+        const unsigned long long t1 = clock64();
+        c_acc += t1 - t0;
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.nb);
       for (int j = 0; j < a.n_pairs; ++j) {
+        if (prof) t0 = clock64();
         mbar_wait(&st_full[st], sph, 113);
+        if (prof) {
+          const unsigned long long t1 = clock64();
+          c_b += t1 - t0;
+        }
         tc_fence_after();
         const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
         const uint64_t b0 = make_desc(smem_u32(sB + static_cast<size_t>(st) * a.stage_bytes), b_lbo, 128);
@@ -191,7 +249,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                                 static_cast<uint32_t>((u - pi) >> (a.stride - 1)) * static_cast<uint32_t>(a.cout);
           const int v = u - a.pad;
           const uint32_t boff = static_cast<uint32_t>((v & (a.Q - 1)) * a.R + 8 + (v >> a.qs));
-          if (elect_one()) mma_f16_ss(d_tmem, a0 + aoff, b0 + boff, idesc, (j | u) ? 1u : 0u);
+          if (!(a.dbg & 2) && elect_one()) mma_f16_ss(d_tmem, a0 + aoff, b0 + boff, idesc, (j | u) ? 1u : 0u);
         }
         __syncwarp();
         if (elect_one()) mma_commit(&st_empty[st]);
@@ -213,9 +271,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         accph ^= 1u;
       }
     }
+    if (prof) {
+      a.prof[blockIdx.x * 8 + 0] = c_acc;
+      a.prof[blockIdx.x * 8 + 1] = c_b;
+      a.prof[blockIdx.x * 8 + 2] = clock64() - c_start;
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
-    const int eg = (static_cast<int>(warp) - 4) >> 2;
+    // Four warpgroups: ew & 1 = accumulator buffer (every other tile), ew >> 1
+    // = which half of the tile's columns.  The accumulator is held while its
+    // columns are drained, so the MMA of tile k+2 waits for the epilogue of
+    // tile k: two warpgroups per buffer halve that hold time (measured: with
+    // one warpgroup per buffer the MMA warp spent most of its time waiting).
+    const int ew = (static_cast<int>(warp) - 4) >> 2;
+    const int eb = ew & 1;
     const int wq = static_cast<int>(warp) & 3;
     const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
     const int pprime = row / a.cout;
@@ -226,48 +295,55 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const bool has_res = a.res_mode != 0 && g8 * 8 < a.res_c;
     const int out_groups = a.cout / 8;
     const int res_groups = a.res_c / 8;
+    const int nch = a.nb / 16;  // 16-column chunks of the tile; this warpgroup takes half
+    const int c_lo = (ew >> 1) * (nch / 2), c_hi = c_lo + nch / 2;
     uint32_t accph = 0;
+    const bool eprof = (a.dbg & 16) && a.prof && warp == 4 && lane == 0;
+    unsigned long long e_wait = 0, e_work = 0, e_start = eprof ? clock64() : 0;
+    int e_tiles = 0;
     pdl_wait();
-    for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+    for (int tile = blockIdx.x + eb * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+      ++e_tiles;
       const PPTile t = pp_tile(a, tile);
       const float bias = s_bias[t.g * a.cout + c];
       const size_t out_plane = static_cast<size_t>(t.p) * out_groups + g8;
       const size_t res_plane = static_cast<size_t>(t.p) * res_groups + g8;
-      const int n_base = t.nt * a.nb + r8;  // + 32*ch + 8*b: this lane's column after the transpose
-      // Shortcut rows of a 32-column chunk (4 positions per lane after the
-      // transpose; maxpool reads 2 rows each) are loaded one chunk ahead, the
-      // first chunk before the accumulator wait, so their latency hides under
-      // the MMAs / the previous chunk's math.
-      uint4 raw[8];
+      const int n_base = t.nt * a.nb + r8;  // + 16*ch + 8*b: this lane's column after the transpose
+      // Shortcut rows of a chunk (2 positions per lane after the transpose;
+      // maxpool reads 2 rows each) are loaded one chunk ahead, the first
+      // before the accumulator wait.
+      uint4 raw[4];
       auto load_res = [&](int ch) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int l = a.ph * (n_base + 32 * ch + 8 * b) + phase;
-          const bool ok = has_res && l < a.lout;
+        for (int b = 0; b < 2; ++b) {
+          const int l = a.ph * (n_base + 16 * ch + 8 * b) + phase;
+          const bool ok = has_res && l < a.lout && !(a.dbg & 32);
+          const uint4 z = make_uint4(0u, 0u, 0u, 0u);
           if (a.res_mode == 2) {
-            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l)))
-                            : make_uint4(0u, 0u, 0u, 0u);
-            raw[2 * b + 1] = ok ? __ldg(reinterpret_cast<const uint4*>(
-                                      a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1)))
-                                : make_uint4(0u, 0u, 0u, 0u);
+            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l))) : z;
+            raw[2 * b + 1] =
+                ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1))) : z;
           } else {
-            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l)))
-                            : make_uint4(0u, 0u, 0u, 0u);
+            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l))) : z;
           }
         }
       };
-      if (a.res_mode) load_res(0);
-      mbar_wait(&acc_full[eg], accph, 120);
+      if (a.res_mode) load_res(c_lo);
+      unsigned long long e0 = eprof ? clock64() : 0;
+      mbar_wait(&acc_full[eb], accph, 120);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eg * a.nb);
-      const int nch = a.nb / 32;
-      for (int ch = 0; ch < nch; ++ch) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 32), r0);
-        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 32 + 16), r1);
-        uint4 rv[4];
+      if (eprof) {
+        const unsigned long long e1 = clock64();
+        e_wait += e1 - e0;
+        e0 = e1;
+      }
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
+      for (int ch = c_lo; ch < c_hi; ++ch) {
+        uint32_t r[16];
+        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 16), r);
+        uint4 rv[2];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < 2; ++b) {
           if (a.res_mode == 2) {
             const __half2* h0 = reinterpret_cast<const __half2*>(&raw[2 * b]);
             const __half2* h1 = reinterpret_cast<const __half2*>(&raw[2 * b + 1]);
@@ -278,39 +354,50 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             rv[b] = a.res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
           }
         }
-        if (a.res_mode && ch + 1 < nch) load_res(ch + 1);
+        if (a.res_mode && ch + 1 < c_hi) load_res(ch + 1);
         tmem_wait_ld();
-        if (ch == nch - 1) {  // accumulator drained: the next tile's MMAs may start
+        if (ch == c_hi - 1) {  // this warpgroup's columns drained
           tc_fence_before();
-          mbar_arrive(&acc_empty[eg]);
+          mbar_arrive(&acc_empty[eb]);
         }
+        if (a.dbg & 1) continue;
+        // (acc + bias) is rounded to fp16 before the transpose; the shortcut
+        // add and ReLU run on half2 (two roundings instead of one: within one
+        // fp16 ulp of the fp32 reference, tests/test_conv_pp_gpu.py).
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          float v[8];
+        for (int b = 0; b < 2; ++b) {
+          uint32_t h[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t bits = (b < 2) ? r0[8 * b + k] : r1[8 * (b - 2) + k];
-            v[k] = __uint_as_float(bits) + bias;
+          for (int k = 0; k < 4; ++k) {
+            const __half2 v2 = __floats2half2_rn(__uint_as_float(r[8 * b + 2 * k]) + bias,
+                                                 __uint_as_float(r[8 * b + 2 * k + 1]) + bias);
+            h[k] = *reinterpret_cast<const uint32_t*>(&v2);
           }
-          transpose8(v, r8);
-          const int l = a.ph * (n_base + 32 * ch + 8 * b) + phase;
+          transpose8_h2(h, r8);
+          const int l = a.ph * (n_base + 16 * ch + 8 * b) + phase;
           if (l < a.out_rows) {
-            const __half2* h2 = reinterpret_cast<const __half2*>(&rv[b]);
+            const __half2* rr = reinterpret_cast<const __half2*>(&rv[b]);
+            const __half2 zero = __float2half2_rn(0.f);
+            const bool valid = l < a.lout;
             uint4 pk;
             __half2* o2 = reinterpret_cast<__half2*>(&pk);
-            const bool valid = l < a.lout;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const float2 f = __half22float2(h2[k]);
-              const float y0 = fmaxf(v[2 * k] + f.x, 0.f);
-              const float y1 = fmaxf(v[2 * k + 1] + f.y, 0.f);
-              o2[k] = valid ? __floats2half2_rn(y0, y1) : __floats2half2_rn(0.f, 0.f);
+              const __half2 y = __hmax2(__hadd2(*reinterpret_cast<const __half2*>(&h[k]), rr[k]), zero);
+              o2[k] = valid ? y : zero;
             }
             *reinterpret_cast<uint4*>(a.out + q_off(out_plane, a.out_qs, a.out_lq, l)) = pk;
           }
         }
       }
+      if (eprof) e_work += clock64() - e0;
       accph ^= 1u;
+    }
+    if (eprof) {
+      a.prof[blockIdx.x * 8 + 3] = e_wait;
+      a.prof[blockIdx.x * 8 + 4] = e_work;
+      a.prof[blockIdx.x * 8 + 5] = clock64() - e_start;
+      a.prof[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(e_tiles);
     }
   }
 
@@ -381,7 +468,7 @@ static EncodeTiledFnPP get_encode_pp() {
 static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const int* fits) {
   static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
   const int cands[3] = {256, 128, 64};
-  const double cost[3] = {1.0, 1.08, 1.3};  // per-column cost of a narrower MMA (smem-read bound below 256)
+  const double cost[3] = {1.0, 1.4, 2.0};  // per-column MMA cost (measured: A is re-read per MMA, N=128 runs ~1.4x slower per column)
   int best = 0;
   double best_t = 1e30;
   for (int k = 0; k < 3; ++k) {
@@ -451,7 +538,10 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   a.R = round_up(8 + a.nb + dr_max, 8);
   a.stage_bytes = static_cast<uint32_t>(2 * a.Q * a.R * 16);
   a.n_stages = static_cast<int>(budget / a.stage_bytes);
-  if (a.n_stages > 4) a.n_stages = 4;
+  {
+    static const int cap = getenv("HB_PP_STAGES") ? atoi(getenv("HB_PP_STAGES")) : 4;
+    if (a.n_stages > cap) a.n_stages = cap;
+  }
   a.nt_per_p = (n_cols + a.nb - 1) / a.nb;
   a.num_tiles = a.P * a.nt_per_p;
   a.tmem_cols = static_cast<uint32_t>(2 * a.nb < 32 ? 32 : 2 * a.nb);
@@ -481,6 +571,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return "conv_pp: cuTensorMapEncodeTiled rejected the activation view";
+  a.dbg = getenv("HB_PP_DBG") ? atoi(getenv("HB_PP_DBG")) : 0;
   return nullptr;
 }
 
@@ -489,7 +580,7 @@ cudaError_t init_pp_kernel() {
 }
 
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st) {
-  return launch_pdl(conv_pp_kernel, dim3(plan.grid), dim3(kConvThreads), plan.smem_bytes, st, plan.tmap, plan.args);
+  return launch_pdl(conv_pp_kernel, dim3(plan.grid), dim3(kPPThreads), plan.smem_bytes, st, plan.tmap, plan.args);
 }
 
 }  // namespace hb

@@ -950,6 +950,11 @@ int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode,
                   res_mode == 2 ? 2 * lin : lout, res_q, nullptr, nullptr, sms);
   int rc = HB_OK;
   unsigned long long* dprof = nullptr;
+  if (!e && kind == KIND_PP && (plan.pp.args.dbg & 16)) {
+    cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * plan.pp.grid);
+    cudaMemset(dprof, 0, sizeof(unsigned long long) * 8 * plan.pp.grid);
+    plan.pp.args.prof = dprof;
+  }
   if (!e && kind == KIND_TC && (plan.tc.args.dbg & 8)) {
     cudaMalloc(&dprof, sizeof(unsigned long long) * 8 * plan.tc.grid);
     cudaMemset(dprof, 0, sizeof(unsigned long long) * 8 * plan.tc.grid);
@@ -975,6 +980,20 @@ int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode,
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaStreamDestroy(st);
+    if (dprof && kind == KIND_PP) {
+      const int grid = plan.pp.grid;
+      std::vector<unsigned long long> h(8 * grid);
+      cudaMemcpy(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost);
+      double sum[8] = {0};
+      for (int i = 0; i < grid; ++i)
+        for (int k = 0; k < 8; ++k) sum[k] += static_cast<double>(h[i * 8 + k]) / grid;
+      const double tiles = static_cast<double>(plan.pp.args.num_tiles) / grid;
+      fprintf(stderr, "[pp prof] nb=%d stages=%d tiles/CTA %.1f | per tile (cycles): mma wait_acc %.0f wait_b %.0f total %.0f | epi(wg0) wait %.0f work %.0f (per its tile, %.1f tiles)\n",
+              plan.pp.args.nb, plan.pp.args.n_stages, tiles, sum[0] / tiles, sum[1] / tiles, sum[2] / tiles,
+              sum[3] / sum[6], sum[4] / sum[6], sum[6]);
+      cudaFree(dprof);
+      dprof = nullptr;
+    }
     if (dprof) {
       std::vector<unsigned long long> h(8 * plan.tc.grid);
       cudaMemcpy(h.data(), dprof, h.size() * 8, cudaMemcpyDeviceToHost);

@@ -108,6 +108,9 @@ struct PPArgs {
   int out_qs, out_lq, out_rows;
   const __half* res;
   int res_mode, res_c, res_qs, res_lq;
+  int dbg;                         // experiments only (HB_PP_DBG): 1 no epilogue math/stores, 2 no MMAs, 4 no B loads,
+                                   // 8 no shortcut L2 prefetch, 16 role cycle counters into prof
+  unsigned long long* prof;        // dbg & 16: per CTA [8]
 };
 struct PPPlan {
   PPArgs args;
