@@ -102,6 +102,10 @@ __device__ __forceinline__ void transpose8_h2(uint32_t (&h)[4], int r8) {
   }
 }
 
+// Shortcut row load (HB_PP_DBG & 64: L2-only ld.global.cg instead of the
+// read-only L1 path).
+__device__ __forceinline__ uint4 ldres_sel(const uint4* p, bool cg) { return cg ? __ldcg(p) : __ldg(p); }
+
 __global__ void __launch_bounds__(kPPThreads, 1)
     conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ PPArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -313,6 +317,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       // maxpool reads 2 rows each) are loaded one chunk ahead, the first
       // before the accumulator wait.
       uint4 raw[4];
+      const bool cg = (a.dbg & 64) != 0;
+      auto ldres = [&](const uint4* p) { return ldres_sel(p, cg); };
       auto load_res = [&](int ch) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
@@ -320,11 +326,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const bool ok = has_res && l < a.lout && !(a.dbg & 32);
           const uint4 z = make_uint4(0u, 0u, 0u, 0u);
           if (a.res_mode == 2) {
-            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l))) : z;
+            raw[2 * b] = ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l))) : z;
             raw[2 * b + 1] =
-                ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1))) : z;
+                ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1))) : z;
           } else {
-            raw[2 * b] = ok ? __ldg(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l))) : z;
+            raw[2 * b] = ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l))) : z;
           }
         }
       };
