@@ -280,10 +280,8 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
     }
   }
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
-                         c->ens_logit, c->ens_sums, st));
-  pr->mark(st, K_AGG, 0.0, 0.0);
-  CK(c, launch_advance(c->wpos, c->hop, st));
-  pr->mark(st, K_ADV, 0.0, 0.0);
+                         c->ens_logit, c->ens_sums, c->wpos, c->hop, st));
+  pr->mark(st, K_AGG, 0.0, 0.0);  // (the cursor advance, K_ADV, is fused into the aggregate)
   return HB_OK;
 }
 

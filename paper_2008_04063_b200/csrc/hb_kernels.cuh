@@ -202,7 +202,8 @@ struct HeadMember {
   float fc_b;
 };
 cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits /*[P][M]*/,
-                             float* ens_prob, float* ens_logit, float* ens_sums /*[2][P]*/, cudaStream_t st);
+                             float* ens_prob, float* ens_logit, float* ens_sums /*[2][P]*/, long long* wpos /*advanced by `advance`, may be null*/,
+                             int advance, cudaStream_t st);
 cudaError_t launch_finalize(const float* sums, int P, int m_total, float* prob, float* logit, cudaStream_t st);
 constexpr int kMaxMembers = 64;
 

@@ -131,11 +131,14 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __rest
                                                         float* __restrict__ member_logits,
                                                         float* __restrict__ ens_prob,
                                                         float* __restrict__ ens_logit,
-                                                        float* __restrict__ ens_sums) {
+                                                        float* __restrict__ ens_sums, long long* wpos,
+                                                        int advance) {
   __shared__ float s_logit[kMaxMembers];
   const int p = blockIdx.x;
   pdl_wait();
   pdl_trigger();
+  // the tick's ring cursor advance rides on the last kernel of the tick
+  if (wpos != nullptr && p == 0 && threadIdx.x == 0) *wpos += advance;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m = warp; m < M; m += 8) {
     const HeadMember hm = mem[m];
@@ -162,10 +165,10 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const HeadMember* __rest
 }
 
 cudaError_t launch_aggregate(const HeadMember* members_dev, int M, int P, float* member_logits, float* ens_prob,
-                             float* ens_logit, float* ens_sums, cudaStream_t st) {
+                             float* ens_logit, float* ens_sums, long long* wpos, int advance, cudaStream_t st) {
   if (M < 1 || M > kMaxMembers) return cudaErrorInvalidValue;
   return launch_pdl(aggregate_kernel, dim3(P), dim3(256), 0, st, members_dev, M, P, member_logits, ens_prob,
-                    ens_logit, ens_sums);
+                    ens_logit, ens_sums, wpos, advance);
 }
 
 // Member-sharded finish: sums[2][P] reduced over ranks -> means over the total popcount.
