@@ -107,7 +107,8 @@ __device__ __forceinline__ void transpose8_h2(uint32_t (&h)[4], int r8) {
 __device__ __forceinline__ uint4 ldres_sel(const uint4* p, bool cg) { return cg ? __ldcg(p) : __ldg(p); }
 
 __global__ void __launch_bounds__(kPPThreads, 1)
-    conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ PPArgs a) {
+    conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ PPArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sB = smem + a.w_bytes;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const uint32_t lane = lane_id();
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmB);
+    if (a.n_res_pairs) prefetch_tmap(&tmX);
     for (int i = 0; i < a.n_stages; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 1);
@@ -175,14 +177,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           loaded_g = t.g;
         }
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
-        for (int j = 0; j < a.n_pairs; ++j) {
+        for (int j = 0; j < a.n_pairs + a.n_res_pairs; ++j) {
           mbar_wait(&st_empty[st], sph ^ 1u, 102);
           if (a.dbg & 4) {
             mbar_arrive(&st_full[st]);
           } else {
             mbar_arrive_expect_tx(&st_full[st], a.stage_bytes);
-            tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmB, &st_full[st], 0, line0, 0,
-                        t.p * planes_per_p + 2 * j);
+            if (j < a.n_pairs)
+              tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmB, &st_full[st], 0, line0, 0,
+                          t.p * planes_per_p + 2 * j);
+            else  // the identity shortcut's rows, same box geometry (x is in this conv's Q-phase layout)
+              tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, &tmX, &st_full[st], 0, line0, 0,
+                          t.p * (a.res_c / 8) + 2 * (j - a.n_pairs));
           }
           if (++st == a.n_stages) {
             st = 0;
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.nb);
-      for (int j = 0; j < a.n_pairs; ++j) {
+      for (int j = 0; j < a.n_pairs + a.n_res_pairs; ++j) {
         if (prof) t0 = clock64();
         mbar_wait(&st_full[st], sph, 113);
         if (prof) {
@@ -245,8 +251,19 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           c_b += t1 - t0;
         }
         tc_fence_after();
-        const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
         const uint64_t b0 = make_desc(smem_u32(sB + static_cast<size_t>(st) * a.stage_bytes), b_lbo, 128);
+        if (j >= a.n_pairs) {
+          // identity shortcut on the tensor core: D[(p', c), n] += x[c, ph*n + p] as one K=16 MMA per
+          // phase p, A = the phase-p window of the selection array Z (ones at (p', c) -> channel c)
+          const uint64_t z0 = make_desc(smem_u32(sW) + a.z_off + static_cast<uint32_t>(j - a.n_pairs) * a.z_pair_bytes,
+                                        a.z_half_bytes, 128);
+          for (int ps = 0; ps < a.ph; ++ps) {
+            if (!(a.dbg & 2) && elect_one())
+              mma_f16_ss(d_tmem, z0 + static_cast<uint32_t>(ps * a.cout), b0 + static_cast<uint32_t>(ps * a.R + 8),
+                         idesc, 1u);
+          }
+        } else {
+        const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
         for (int u = 0; u < a.U; ++u) {
           const int pi = (a.stride == 2) ? (u & 1) : 0;
           const uint32_t aoff = static_cast<uint32_t>(pi) * a.w_par16 +
@@ -254,6 +271,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           const int v = u - a.pad;
           const uint32_t boff = static_cast<uint32_t>((v & (a.Q - 1)) * a.R + 8 + (v >> a.qs));
           if (!(a.dbg & 2) && elect_one()) mma_f16_ss(d_tmem, a0 + aoff, b0 + boff, idesc, (j | u) ? 1u : 0u);
+        }
         }
         __syncwarp();
         if (elect_one()) mma_commit(&st_empty[st]);
@@ -425,14 +443,21 @@ bool pp_shape_ok(int cin, int cout, int stride) {
   return stride == 1 || stride == 2;
 }
 
-size_t pp_wbytes(int cin, int cout, int stride) {
+static size_t pp_conv_wbytes(int cin, int cout, int stride) {
   return static_cast<size_t>(cin / 8) * stride * pp_taps_per_parity(cout, stride) * cout * 16;
+}
+// Identity-shortcut selection array per 16-channel shortcut group: [half][z][16 B],
+// z in [0, (2ph-1)*cout): row (ph-1)*cout + c holds a one at channel c - (16 jr + 8 half).
+static size_t pp_z_half_bytes(int cout) { return static_cast<size_t>(2 * pp_phases(cout) - 1) * cout * 16; }
+
+size_t pp_wbytes(int cin, int cout, int stride, int zc) {
+  return pp_conv_wbytes(cin, cout, stride) + static_cast<size_t>(zc / 16) * 2 * pp_z_half_bytes(cout);
 }
 
 // Weight image [pair j][half h][parity pi][entry e][cout][8 fp16]:
 // entry e of parity pi holds tap stride*(e - (ph-1)) + pi (zero outside [0,16)),
-// channels 16j + 8h .. +7.
-void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) {
+// channels 16j + 8h .. +7; then (zc > 0) the shortcut selection arrays.
+void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst, int zc) {
   const int ph = pp_phases(cout), na = pp_taps_per_parity(cout, stride);
   size_t o = 0;
   for (int j = 0; j < cin / 16; ++j)
@@ -449,6 +474,17 @@ void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* ds
               std::memcpy(&bits, &hv, 2);
               dst[o++] = bits;
             }
+        }
+  const __half one = __float2half_rn(1.f);
+  uint16_t one_bits;
+  std::memcpy(&one_bits, &one, 2);
+  const int zrows = (2 * ph - 1) * cout, z0 = (ph - 1) * cout;
+  for (int jr = 0; jr < zc / 16; ++jr)
+    for (int h = 0; h < 2; ++h)
+      for (int z = 0; z < zrows; ++z)
+        for (int k = 0; k < 8; ++k) {
+          const int c = z - z0;
+          dst[o++] = (c >= 0 && c < cout && c == 16 * jr + 8 * h + k) ? one_bits : 0;
         }
 }
 
@@ -494,7 +530,7 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const int* f
 
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
-                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms) {
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc) {
   std::memset(plan, 0, sizeof(*plan));
   if (G < 1 || G > kMaxGroup || Pm < 1) return "conv_pp: bad group shape";
   if (!pp_shape_ok(cin, cout, stride)) return "conv_pp: unsupported layer shape";
@@ -522,8 +558,18 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   a.w_par16 = static_cast<uint32_t>(na * cout);  // one parity array, 16-B units
   a.w_half_bytes = static_cast<uint32_t>(stride * na * cout * 16);
   a.w_pair_bytes = 2 * a.w_half_bytes;
-  a.w_bytes = static_cast<uint32_t>(pp_wbytes(cin, cout, stride));
-  a.w_stride = pp_wbytes(cin, cout, stride);
+  // Identity shortcut as MMAs when the image carries Z for it and x is in this
+  // conv's input layout.  Measured (192 rows, L=7500): 32 channels 68 -> 51 us;
+  // 64 channels 115 -> 148 us (the 64-channel weights leave 3 B stages for 8
+  // loads per tile, and the epilogue path is cheaper there), so only ph >= 4.
+  const bool res_mma = res && res_mode == 1 && res_q == a.ph && a.ph >= 4 && res_c % 16 == 0 && zc == res_c &&
+                       !(getenv("HB_PP_RES_EPI") && atoi(getenv("HB_PP_RES_EPI")));
+  a.n_res_pairs = res_mma ? res_c / 16 : 0;
+  a.z_off = static_cast<uint32_t>(pp_conv_wbytes(cin, cout, stride));
+  a.z_half_bytes = static_cast<uint32_t>(pp_z_half_bytes(cout));
+  a.z_pair_bytes = 2 * a.z_half_bytes;
+  a.w_bytes = static_cast<uint32_t>(pp_wbytes(cin, cout, stride, res_mma ? zc : 0));
+  a.w_stride = pp_wbytes(cin, cout, stride, zc);
   a.in_lq = lq_Q(lin, a.Q);
   a.out_qs = ilog2(out_q);
   a.out_lq = lq_Q(lout, out_q);
@@ -556,7 +602,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   a.bias_stride = static_cast<int>(bias_len(cout));
   a.out = out;
   a.res = res;
-  a.res_mode = res ? res_mode : 0;
+  a.res_mode = (res && !res_mma) ? res_mode : 0;  // the epilogue's share of the shortcut
   a.res_c = res ? res_c : 0;
   a.res_qs = res ? ilog2(res_q) : 0;
   a.res_lq = res ? lq_Q(res_len, res_q) : 0;
@@ -577,6 +623,17 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) return "conv_pp: cuTensorMapEncodeTiled rejected the activation view";
+  if (res_mma) {  // x: {lines, lq/8, Q = ph phases, P*res_c/8 planes}, the same box as a B stage
+    const cuuint64_t xlq = static_cast<cuuint64_t>(lq_Q(res_len, res_q));
+    const cuuint64_t xd[4] = {64, xlq / 8, static_cast<cuuint64_t>(res_q), static_cast<cuuint64_t>(a.P) * (res_c / 8)};
+    const cuuint64_t xs[3] = {128, xlq * 16, static_cast<cuuint64_t>(res_q) * xlq * 16};
+    const CUresult rx = enc(&plan->tmapX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half*>(res), xd, xs, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rx != CUDA_SUCCESS) return "conv_pp: cuTensorMapEncodeTiled rejected the shortcut view";
+  } else {
+    plan->tmapX = plan->tmap;  // unused
+  }
   a.dbg = getenv("HB_PP_DBG") ? atoi(getenv("HB_PP_DBG")) : 0;
   return nullptr;
 }
@@ -586,7 +643,8 @@ cudaError_t init_pp_kernel() {
 }
 
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st) {
-  return launch_pdl(conv_pp_kernel, dim3(plan.grid), dim3(kPPThreads), plan.smem_bytes, st, plan.tmap, plan.args);
+  return launch_pdl(conv_pp_kernel, dim3(plan.grid), dim3(kPPThreads), plan.smem_bytes, st, plan.tmap, plan.tmapX,
+                    plan.args);
 }
 
 }  // namespace hb

@@ -63,11 +63,14 @@ int layer_kind(const LayerSpec& L) {
 }
 // Input layout (phases Q) a conv of `kind` reads: K4 reads I (s=1) / S (s=2).
 int layer_in_q(const LayerSpec& L, int kind) { return kind == KIND_PP ? L.stride * pp_phases(L.cout) : L.stride; }
+// K4b images of identity-shortcut layers also carry the shortcut selection
+// arrays (the shortcut then runs as MMAs when x's layout allows, conv_pp.cu).
+int layer_zc(const LayerSpec& L) { return (L.res_mode == 1 && L.res_c % 16 == 0 && L.res_c <= L.cout) ? L.res_c : 0; }
 size_t layer_wbytes(const LayerSpec& L, int kind) {
-  return kind == KIND_PP ? pp_wbytes(L.cin, L.cout, L.stride) : wpack_bytes(L.cin, L.cout);
+  return kind == KIND_PP ? pp_wbytes(L.cin, L.cout, L.stride, layer_zc(L)) : wpack_bytes(L.cin, L.cout);
 }
 void layer_pack(const LayerSpec& L, int kind, const float* w, uint16_t* dst) {
-  if (kind == KIND_PP) pp_pack_weights(w, L.cin, L.cout, L.stride, dst);
+  if (kind == KIND_PP) pp_pack_weights(w, L.cin, L.cout, L.stride, dst, layer_zc(L));
   else pack_weights(w, L.cin, L.cout, L.stride, dst);
 }
 // Rows per activation plane that hold any Q-phase layout (Q <= 32) of length L.
@@ -429,7 +432,7 @@ int build_selection(hb_ctx* c) {
         if (plan.kind == KIND_PP) {
           e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src], act[dst], out_q,
                       g.wpack[li - 1], g.bias[li - 1], res, conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q,
-                      c->num_sms);
+                      c->num_sms, layer_zc(L));
         } else {
           e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
                         L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
@@ -861,7 +864,7 @@ int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const fl
   if (kind == KIND_PP)
     e = plan_pp(&plan.pp, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
                 static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
-                res_len > 0 ? res_len : lout, res_q, sms);
+                res_len > 0 ? res_len : lout, res_q, sms, layer_zc(spec));
   else
     e = plan_conv(&plan.tc, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
                   static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
@@ -940,7 +943,7 @@ int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode,
     e = plan_pp(&plan.pp, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
                 static_cast<__half*>(dout), out_q, static_cast<uint8_t*>(dw), static_cast<float*>(db),
                 res_mode ? static_cast<const __half*>(dres) : nullptr, res_mode, cin < cout ? cin : cout,
-                res_mode == 2 ? 2 * lin : lout, res_q, sms);
+                res_mode == 2 ? 2 * lin : lout, res_q, sms, layer_zc(spec));
   else
     e = plan_conv(&plan.tc, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(din),
                   static_cast<__half*>(dout), out_q, static_cast<uint8_t*>(dw), static_cast<float*>(db),

@@ -92,6 +92,8 @@ struct PPArgs {
   int cin, cout, stride, pad, lin, lout;
   int ph, Q, qs, U;                // output phases 128/cout, input phases stride*ph = 1 << qs, shifts
   int n_pairs;                     // 16-channel K groups (cin / 16)
+  int n_res_pairs;                 // identity shortcut on the tensor core: 16-channel groups of x (0 = epilogue)
+  uint32_t z_off, z_half_bytes, z_pair_bytes;  // shortcut selection arrays Z in the weight image
   uint32_t w_par16;                // one tap-parity array, 16-B units
   uint32_t w_half_bytes, w_pair_bytes, w_bytes;  // weight image: [pair][half][parity][entry][cout][16 B]
   size_t w_stride;                 // bytes per member image
@@ -115,16 +117,19 @@ struct PPArgs {
 struct PPPlan {
   PPArgs args;
   CUtensorMap tmap;                // input view {8-row lines, lines, Q phases, planes}
+  CUtensorMap tmapX;               // shortcut view (same box) when the shortcut runs as MMAs
   int grid;
   uint32_t smem_bytes;
 };
 bool pp_shape_ok(int cin, int cout, int stride);
 int pp_phases(int cout);           // 128 / cout; the input of a pp conv is in Q = stride * phases layout
-size_t pp_wbytes(int cin, int cout, int stride);
-void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */);
+// zc > 0: the image also carries the identity-shortcut selection arrays for zc
+// shortcut channels (appended; plan_pp uses them when the shortcut's layout allows).
+size_t pp_wbytes(int cin, int cout, int stride, int zc = 0);
+void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */, int zc = 0);
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
-                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms);
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc = 0);
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
 cudaError_t init_pp_kernel();
 

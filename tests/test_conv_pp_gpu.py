@@ -67,8 +67,14 @@ PP_CASES = [
 ]
 
 
+@pytest.mark.parametrize("res_layout", ["native", "other"])
 @pytest.mark.parametrize("cin,cout,lin,stride,res_mode,P,out_q", PP_CASES)
-def test_pp_conv_matches_fp32(cin, cout, lin, stride, res_mode, P, out_q):
+def test_pp_conv_matches_fp32(cin, cout, lin, stride, res_mode, P, out_q, res_layout):
+    """res_layout "native": the identity shortcut is in this conv's own Q-phase
+    layout (Q = 128/cout) and runs as selection MMAs on the tensor core;
+    "other": a different Q, read by the epilogue."""
+    if res_mode == 0 and res_layout == "other":
+        pytest.skip("no shortcut")
     g = torch.Generator().manual_seed(cin * 5 + cout + lin + stride + out_q)
     x = torch.relu(_rand((P, cin, lin), g))
     w = _rand((cout, cin, 16), g, (2.0 / (cin * 16)) ** 0.5)
@@ -76,7 +82,8 @@ def test_pp_conv_matches_fp32(cin, cout, lin, stride, res_mode, P, out_q):
     res = None
     if res_mode == 1:
         res = torch.relu(_rand((P, min(cin, cout), -(-lin // stride)), g))
-    out, lout = run_q(x, w, b, stride, K_PP, res, res_mode, res_q=4 if res is not None else 1, out_q=out_q)
+    rq = (128 // cout if res_layout == "native" else (2 if 128 // cout != 2 else 4)) if res is not None else 1
+    out, lout = run_q(x, w, b, stride, K_PP, res, res_mode, res_q=rq, out_q=out_q)
     ref = ref_conv(x, w, b, stride, res, res_mode)
     got = from_q(out, cout, lout, out_q).float().cpu()
     err = (got - ref).abs()
