@@ -121,7 +121,8 @@ int hb_time_tick(hb_ctx* ctx, int reps, float* median_ms);
 int hb_last_windows(hb_ctx* ctx, float* raw, float* stats, void* stream);
 /* Eagerly launch one tick kernel-by-kernel with a CUDA event after every
  * launch (same kernels and order as the graph) and report, per launch: kind
- * (0 ingest/window, 1 stem, 2 tcgen05 conv, 3 aggregate + cursor advance),
+ * (0 ingest/window, 1 stem, 2 tcgen05 conv K4, 3 aggregate + cursor advance,
+ * 5 tcgen05 polyphase conv K4b),
  * device milliseconds, algorithmic FLOPs and bytes.  Returns the number of
  * launches (>= 0) or -status.  Advances the stream cursor like a tick. */
 int hb_profile_tick(hb_ctx* ctx, void* stream, int cap, int* kinds, float* ms, double* flops, double* bytes);

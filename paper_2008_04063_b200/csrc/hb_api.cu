@@ -211,7 +211,7 @@ void free_member(Member& m) {
 }
 
 // Kernel kinds reported by hb_profile_tick.
-enum { K_INGEST = 0, K_STEM = 1, K_CONV = 2, K_AGG = 3, K_ADV = 4 };
+enum { K_INGEST = 0, K_STEM = 1, K_CONV = 2, K_AGG = 3, K_ADV = 4, K_CONV_PP = 5 };
 
 struct ProfRec {
   std::vector<cudaEvent_t>* ev = nullptr;  // event recorded after every launch
@@ -267,8 +267,9 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
       size_t pi = g.plan0[ch];
       for (size_t li = 1; li < g.layers.size(); ++li) {
         const LayerSpec& L = g.layers[li];
+        const int kk = c->plans[pi].kind == KIND_PP ? K_CONV_PP : K_CONV;
         CK(c, launch_layer(c->plans[pi++], ms));
-        pr->mark(ms, K_CONV, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
+        pr->mark(ms, kk, rows * 2.0 * L.cin * L.cout * kTaps * L.lout,
                  rows * 2.0 * (static_cast<double>(L.cin) * L.lin +
                                (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
                                (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0)));

@@ -1,6 +1,7 @@
-"""DRAM traffic of the conv kernel over one c2 tick, from an ncu CSV
+"""DRAM traffic of the conv kernels over one c2 tick, from an ncu CSV
 (--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
--k regex:conv_tc) -> profiles/ncu_conv_summary.json (read by bench.py)."""
+-k regex:conv_) -> profiles/ncu_conv_summary.json (read by bench.py): per
+kernel (K4b = conv_pp, K4 = conv_tc) and both together."""
 import collections
 import csv
 import json
@@ -14,14 +15,19 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3
 for r in data:
     per[r[ii]][r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
     per[r[ii]]["kernel"] = r[ki].split("(")[0]
-launches = [v for v in per.values() if "conv_tc" in v["kernel"]]
-rd = sum(v.get("dram__bytes_read.sum", 0) for v in launches)
-wr = sum(v.get("dram__bytes_write.sum", 0) for v in launches)
-ns = sum(v.get("gpu__time_duration.sum", 0) for v in launches)
-out = {"source": sys.argv[1], "launches": len(launches), "dram_read_bytes_per_tick": rd, "dram_write_bytes_per_tick": wr,
-       "dram_bytes_per_tick": rd + wr, "dram_bytes_per_launch": (rd + wr) / max(1, len(launches)),
-       "ncu_conv_ms_per_tick_cold": ns / 1e6,
-       "note": "ncu serialises launches with cold caches; compare shares, not absolute times"}
+def summ(name):
+    launches = [v for v in per.values() if name in v["kernel"]]
+    rd = sum(v.get("dram__bytes_read.sum", 0) for v in launches)
+    wr = sum(v.get("dram__bytes_write.sum", 0) for v in launches)
+    ns = sum(v.get("gpu__time_duration.sum", 0) for v in launches)
+    return {"launches": len(launches), "dram_read_bytes_per_tick": rd, "dram_write_bytes_per_tick": wr,
+            "dram_bytes_per_tick": rd + wr, "dram_bytes_per_launch": (rd + wr) / max(1, len(launches)),
+            "ncu_ms_per_tick_cold": ns / 1e6}
+
+
+out = {"source": sys.argv[1], "note": "ncu serialises launches with cold caches; compare shares, not absolute times",
+       "conv_pp": summ("conv_pp"), "conv_tc": summ("conv_tc"), "all_conv": summ("conv_")}
+out.update(out["conv_pp"])  # the dominant kernel (K4b) at top level
 if len(sys.argv) > 2:
     json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))
