@@ -149,6 +149,10 @@ struct hb_ctx {
   float* ens_prob = nullptr;
   float* ens_logit = nullptr;
   float* ens_sums = nullptr;  // [2][P]: sum of member sigmoids, sum of member logits
+  // member_logits [P][M], ens_prob [P], ens_logit [P] are one device block;
+  // graph_io = the tick graph + one D2H of that block into pinned h_out
+  float* h_out = nullptr;
+  cudaGraphExec_t graph_io = nullptr;
   std::vector<LayerPlan> plans;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
@@ -175,6 +179,10 @@ cudaStream_t pick(hb_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) 
 void free_selection(hb_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   c->graph = nullptr;
+  if (c->graph_io) cudaGraphExecDestroy(c->graph_io);
+  c->graph_io = nullptr;
+  if (c->h_out) cudaFreeHost(c->h_out);
+  c->h_out = nullptr;
   for (auto& a : c->act) cudaFree(a);
   c->act.clear();
   for (auto& g : c->groups) {
@@ -192,9 +200,7 @@ void free_selection(hb_ctx* c) {
   c->ev.clear();
   c->act_bytes = 0;
   if (c->d_heads) cudaFree(c->d_heads);
-  if (c->member_logits) cudaFree(c->member_logits);
-  if (c->ens_prob) cudaFree(c->ens_prob);
-  if (c->ens_logit) cudaFree(c->ens_logit);
+  if (c->member_logits) cudaFree(c->member_logits);  // (ens_prob / ens_logit live in the same block)
   if (c->ens_sums) cudaFree(c->ens_sums);
   c->d_heads = nullptr;
   c->member_logits = c->ens_prob = c->ens_logit = c->ens_sums = nullptr;
@@ -359,9 +365,11 @@ int build_selection(hb_ctx* c) {
   for (auto& s2 : c->side) CK(c, cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
   c->ev.resize(1 + c->lanes);
   for (auto& e : c->ev) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CK(c, cudaMalloc(&c->member_logits, sizeof(float) * c->P * M));
-  CK(c, cudaMalloc(&c->ens_prob, sizeof(float) * c->P));
-  CK(c, cudaMalloc(&c->ens_logit, sizeof(float) * c->P));
+  const size_t out_floats = static_cast<size_t>(c->P) * (M + 2);
+  CK(c, cudaMalloc(&c->member_logits, sizeof(float) * out_floats));
+  c->ens_prob = c->member_logits + static_cast<size_t>(c->P) * M;
+  c->ens_logit = c->ens_prob + c->P;
+  CK(c, cudaHostAlloc(&c->h_out, sizeof(float) * out_floats, cudaHostAllocDefault));
   CK(c, cudaMalloc(&c->ens_sums, sizeof(float) * 2 * c->P));
   std::vector<HeadMember> heads(M);
   for (auto& g : c->groups) {
@@ -463,6 +471,23 @@ int build_selection(hb_ctx* c) {
   CK(c, ec);
   CK(c, cudaGraphInstantiate(&c->graph, g, 0));
   cudaGraphDestroy(g);
+  {  // the same tick + one D2H of the output block into pinned h_out (hb_tick with host outputs)
+    cudaGraph_t gio;
+    CK(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int rc2 = enqueue_tick(c, cap);
+    const cudaError_t e2 = rc2 == HB_OK ? cudaMemcpyAsync(c->h_out, c->member_logits, sizeof(float) * out_floats,
+                                                           cudaMemcpyDeviceToHost, cap)
+                                        : cudaSuccess;
+    cudaError_t ec2 = cudaStreamEndCapture(cap, &gio);
+    if (rc2 != HB_OK) {
+      cudaStreamDestroy(cap);
+      return rc2;
+    }
+    CK(c, e2);
+    CK(c, ec2);
+    CK(c, cudaGraphInstantiate(&c->graph_io, gio, 0));
+    cudaGraphDestroy(gio);
+  }
   cudaStreamDestroy(cap);
   c->dirty = false;
   return HB_OK;
@@ -691,25 +716,18 @@ int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_pr
   if (rc) return rc;
   if (samples)
     CK(c, cudaMemcpyAsync(c->staged, samples, sizeof(float) * c->P * c->leads * c->hop, cudaMemcpyHostToDevice, st));
+  const bool host_out = member_logits || ens_prob || ens_mean_logit;
   CK(c, cudaEventRecord(c->t0, st));
-  CK(c, cudaGraphLaunch(c->graph, st));
+  CK(c, cudaGraphLaunch(host_out ? c->graph_io : c->graph, st));
   CK(c, cudaEventRecord(c->t1, st));
   c->timed = true;
-  const size_t M = c->selected.size();
-  bool any = false;
-  if (member_logits) {
-    CK(c, cudaMemcpyAsync(member_logits, c->member_logits, sizeof(float) * c->P * M, cudaMemcpyDeviceToHost, st));
-    any = true;
+  if (host_out) {
+    CK(c, cudaStreamSynchronize(st));
+    const size_t P = c->P, M = c->selected.size();
+    if (member_logits) std::memcpy(member_logits, c->h_out, sizeof(float) * P * M);
+    if (ens_prob) std::memcpy(ens_prob, c->h_out + P * M, sizeof(float) * P);
+    if (ens_mean_logit) std::memcpy(ens_mean_logit, c->h_out + P * M + P, sizeof(float) * P);
   }
-  if (ens_prob) {
-    CK(c, cudaMemcpyAsync(ens_prob, c->ens_prob, sizeof(float) * c->P, cudaMemcpyDeviceToHost, st));
-    any = true;
-  }
-  if (ens_mean_logit) {
-    CK(c, cudaMemcpyAsync(ens_mean_logit, c->ens_logit, sizeof(float) * c->P, cudaMemcpyDeviceToHost, st));
-    any = true;
-  }
-  if (any) CK(c, cudaStreamSynchronize(st));
   return HB_OK;
 }
 

@@ -74,6 +74,8 @@ class EnsembleEngine:
         h = C.c_void_p()
         _lib.check(L.hb_create(device, C.byref(cfg), C.byref(h)))
         self._h = h
+        self._hb_tick = L.hb_tick
+        self._out_ptrs = None  # (out, member_logits, ens_prob, ens_mean_logit addresses) of the last TickResult
         self._registered: set = set()
         to_register = range(zoo.n) if register == "all" else selector.indices()
         for i in to_register:
@@ -105,6 +107,7 @@ class EnsembleEngine:
             _lib.check(_lib.lib().hb_set_selector(self._h, bits, b.n), self._h)
             self.selector = b
             self.member_ids = tuple(self.zoo.profiles[i].id for i in b.indices())
+            self._out_ptrs = None
 
     # ------------------------------------------------------------------ data path
     def _check_block(self, samples, n) -> np.ndarray:
@@ -122,15 +125,33 @@ class EnsembleEngine:
             _lib.check(_lib.lib().hb_ingest(self._h, _lib.fptr(a), a.shape[2], None), self._h)
 
     def tick(self, samples, out: TickResult | None = None) -> TickResult:
-        """Append one hop [P, leads, hop] and score every patient's latest window."""
-        a = self._check_block(samples, self.hop)
-        M = self.selector.popcount
+        """Append one hop [P, leads, hop] and score every patient's latest window.
+
+        Per-call host overhead is kept to a few microseconds: a float32
+        C-contiguous block of the right shape is passed as is, and the output
+        buffers' addresses are cached per reused ``out`` (the serving loop and
+        the benchmark reuse one TickResult)."""
+        if (type(samples) is np.ndarray and samples.dtype == np.float32 and samples.flags.c_contiguous
+                and samples.shape == (self.patients, self.leads, self.hop)):
+            a = samples
+        else:
+            a = self._check_block(samples, self.hop)
         if out is None:
+            M = self.selector.popcount
             out = TickResult(self.member_ids, np.empty((self.patients, M), np.float32),
                              np.empty(self.patients, np.float32), np.empty(self.patients, np.float32))
+        cached = self._out_ptrs
+        if cached is None or cached[0] is not out:
+            for arr, shape in ((out.member_logits, (self.patients, self.selector.popcount)),
+                               (out.ens_prob, (self.patients,)), (out.ens_mean_logit, (self.patients,))):
+                if arr.dtype != np.float32 or not arr.flags.c_contiguous or arr.shape != shape:
+                    raise ValueError(f"output buffers must be C-contiguous float32 of shape {shape}")
+            cached = self._out_ptrs = (out, out.member_logits.ctypes.data, out.ens_prob.ctypes.data,
+                                       out.ens_mean_logit.ctypes.data)
         with self._lock:
-            _lib.check(_lib.lib().hb_tick(self._h, _lib.fptr(a), _lib.fptr(out.member_logits),
-                                          _lib.fptr(out.ens_prob), _lib.fptr(out.ens_mean_logit), None), self._h)
+            rc = self._hb_tick(self._h, a.ctypes.data, cached[1], cached[2], cached[3], None)
+        if rc:
+            _lib.check(rc, self._h)
         return out
 
     def stage_device(self, dev_ptr: int, stream: int | None = None) -> None:
