@@ -267,7 +267,7 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
     const double rows = static_cast<double>(c->Pc) * G;
     const LayerSpec& s0 = g.layers[0];
     for (int ch = 0; ch < c->n_chunks; ++ch) {
-      CK(c, launch_stem(g.stem[ch].data(), G, c->W, c->Pc, c->W, layer_in_q(g.layers[1], g.kind[1]), s0.cout,
+      CK(c, launch_stem(g.stem[ch].data(), G, round_up(c->W, 8), c->Pc, c->W, layer_in_q(g.layers[1], g.kind[1]), s0.cout,
                         s0.pad, c->act[3 * ln], ms));
       pr->mark(ms, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
       size_t pi = g.plan0[ch];
@@ -350,7 +350,7 @@ int build_selection(hb_ctx* c) {
   c->n_chunks = (c->P + c->Pc - 1) / c->Pc;
   c->P_pad = c->n_chunks * c->Pc;
   {  // normalised windows [leads][P_pad][W]; rows past P stay zero (padding beds of the last chunk)
-    const size_t xb = static_cast<size_t>(c->leads) * c->P_pad * c->W * sizeof(__half);
+    const size_t xb = static_cast<size_t>(c->leads) * c->P_pad * round_up(c->W, 8) * sizeof(__half);
     CK(c, cudaMalloc(&c->xn, xb));
     CK(c, cudaMemset(c->xn, 0, xb));
   }
@@ -406,7 +406,8 @@ int build_selection(hb_ctx* c) {
       CK(c, cudaMemcpy(g.fc_w + c_last * k, m.fc_w, sizeof(float) * c_last, cudaMemcpyDeviceToDevice));
       for (int ch = 0; ch < c->n_chunks; ++ch)
         g.stem[ch].push_back(
-            {c->xn + (static_cast<size_t>(m.lead) * c->P_pad + static_cast<size_t>(ch) * c->Pc) * c->W, m.stem_w,
+            {c->xn + (static_cast<size_t>(m.lead) * c->P_pad + static_cast<size_t>(ch) * c->Pc) * round_up(c->W, 8),
+             m.stem_w,
              m.stem_b});
       heads[g.mi[k]] = {g.head_partial + static_cast<size_t>(k) * c->P_pad * g.head_mt, g.head_mt,
                         1.f / static_cast<float>(g.layers.back().lout), m.fc_b};
@@ -1053,11 +1054,18 @@ int hb_op_stem_q(const void* xn, int P, int L, const float* w_host, const float*
   CK(none, cudaMemcpy(dw, w_host, sizeof(float) * cout * kTaps, cudaMemcpyHostToDevice));
   CK(none, cudaMalloc(&db, sizeof(float) * cout));
   CK(none, cudaMemcpy(db, b_host, sizeof(float) * cout, cudaMemcpyHostToDevice));
-  const StemMember sm{static_cast<const __half*>(xn), dw, db};
-  cudaError_t ce = launch_stem(&sm, 1, L, P, L, out_q, cout, tot / 2, static_cast<__half*>(out), st);
+  // the stem's TMA view needs 16-B aligned rows: stage the [P][L] windows with a padded stride
+  const int Lp = round_up(L, 8);
+  __half* xp = nullptr;
+  CK(none, cudaMalloc(&xp, sizeof(__half) * P * Lp));
+  CK(none, cudaMemcpy2DAsync(xp, sizeof(__half) * Lp, xn, sizeof(__half) * L, sizeof(__half) * L, P,
+                             cudaMemcpyDeviceToDevice, st));
+  const StemMember sm{xp, dw, db};
+  cudaError_t ce = launch_stem(&sm, 1, Lp, P, L, out_q, cout, tot / 2, static_cast<__half*>(out), st);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
   cudaFree(dw);
   cudaFree(db);
+  cudaFree(xp);
   if (ce != cudaSuccess) return fail(none, HB_E_CUDA, cudaGetErrorString(ce));
   return HB_OK;
 }

@@ -195,7 +195,7 @@ cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int
 // raw gathered window [P][leads][window] fp32, stats (optional) mean/std.
 cudaError_t launch_ingest_window(const float* staged /*[P][leads][n_new]*/, float* ring /*[P][leads][R]*/,
                                  const long long* wpos, int P, int leads, int n_new, int R, int window,
-                                 __half* xn /*[leads][xn_rows][window]*/, int xn_rows, float* raw_out,
+                                 __half* xn /*[leads][xn_rows][roundup(window, 8)]*/, int xn_rows, float* raw_out,
                                  float* stats, cudaStream_t st);
 cudaError_t launch_advance(long long* wpos, int n, cudaStream_t st);
 

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
                                                                     float* __restrict__ ring,
                                                                     const long long* __restrict__ wpos_p, int P,
                                                                     int leads, int n_new, int R, int W,
-                                                                    __half* __restrict__ xn, int xn_rows,
+                                                                    __half* __restrict__ xn, int xn_rows, int xn_stride,
                                                                     float* __restrict__ raw_out,
                                                                     float* __restrict__ stats) {
   extern __shared__ float win[];  // [W] when gathering
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   const float var = block_sum(sq, red) / static_cast<float>(W);
   const float sd = sqrtf(var);
   const float rstd = 1.f / fmaxf(sd, 1e-6f);
-  __half* dst = xn + (static_cast<size_t>(lead) * xn_rows + p) * W;
+  __half* dst = xn + (static_cast<size_t>(lead) * xn_rows + p) * xn_stride;
   if ((W & 1) == 0) {
     __half2* d2 = reinterpret_cast<__half2*>(dst);
     for (int i = threadIdx.x; i < W / 2; i += blockDim.x)
@@ -108,9 +108,10 @@ __global__ void advance_kernel(long long* wpos, int n) {
 cudaError_t launch_ingest_window(const float* staged, float* ring, const long long* wpos, int P, int leads,
                                  int n_new, int R, int window, __half* xn, int xn_rows, float* raw_out, float* stats,
                                  cudaStream_t st) {
+  const int xn_stride = round_up(window, 8);  // 16-B aligned rows (the stem's TMA view)
   const size_t smem = xn ? static_cast<size_t>(window) * sizeof(float) : 0;
   return launch_pdl(ingest_window_kernel, dim3(P * leads), dim3(kWinThreads), smem, st, staged, ring, wpos, P, leads,
-                    n_new, R, window, xn, xn_rows, raw_out, stats);
+                    n_new, R, window, xn, xn_rows, xn_stride, raw_out, stats);
 }
 
 cudaError_t init_stream_kernels() {
