@@ -95,6 +95,17 @@ int hb_ingest(hb_ctx* ctx, const float* samples, int n_per_stream, void* stream)
 int hb_tick(hb_ctx* ctx, const float* samples, float* member_logits, float* ens_prob, float* ens_mean_logit,
             void* stream);
 
+/* Pipelined form of hb_tick with host outputs: hb_tick_submit enqueues the
+ * tick (H2D of `samples`, the tick graph, one D2H of the outputs into the
+ * context's pinned slot `slot` in {0, 1}) and returns; hb_tick_collect waits
+ * for that slot and copies the outputs (same meaning as hb_tick's).  A caller
+ * may submit tick t+1 before collecting tick t, so the device never idles
+ * between ticks on the host round trip.  Submitting into a slot that still
+ * holds an uncollected tick -> HB_E_STATE.  Ticks run in submission order on
+ * `stream`; use one stream per context. */
+int hb_tick_submit(hb_ctx* ctx, const float* samples, int slot, void* stream);
+int hb_tick_collect(hb_ctx* ctx, int slot, float* member_logits, float* ens_prob, float* ens_mean_logit);
+
 /* Device-resident variants (benchmarks, zero-copy callers): copy a device
  * buffer [P][n_leads][hop] into the staging area; outputs stay on device. */
 int hb_stage_device(hb_ctx* ctx, const float* dev_samples, void* stream);

@@ -46,6 +46,8 @@ _SIGS = {
     "hb_selected": (C.c_int, [_P, C.POINTER(C.c_int), C.c_int]),
     "hb_ingest": (C.c_int, [_P, _F, C.c_int, _P]),
     "hb_tick": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "hb_tick_submit": (C.c_int, [_P, _P, C.c_int, _P]),
+    "hb_tick_collect": (C.c_int, [_P, C.c_int, _P, _P, _P]),
     "hb_stage_device": (C.c_int, [_P, _P, _P]),
     "hb_tick_device": (C.c_int, [_P, _P]),
     "hb_device_outputs": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),

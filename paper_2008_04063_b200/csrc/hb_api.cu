@@ -126,7 +126,10 @@ struct hb_ctx {
   double act_budget = 64e9;
   cudaStream_t own = nullptr;
   float* ring = nullptr;
-  float* staged = nullptr;   // [P][leads][hop]
+  float* staged = nullptr;   // [P][leads][hop]: the buffer the tick graph being captured reads
+  float* staged_io[2] = {nullptr, nullptr};  // per submit slot (staged_io[0] == the default staged)
+  cudaStream_t copy = nullptr;               // submit's H2D runs here, overlapping the previous tick
+  cudaEvent_t h2d_done[2] = {nullptr, nullptr};
   float* prefill = nullptr;  // [P][leads][R]
   long long* wpos = nullptr;
   __half* xn = nullptr;      // [leads][P][W]
@@ -150,9 +153,12 @@ struct hb_ctx {
   float* ens_logit = nullptr;
   float* ens_sums = nullptr;  // [2][P]: sum of member sigmoids, sum of member logits
   // member_logits [P][M], ens_prob [P], ens_logit [P] are one device block;
-  // graph_io = the tick graph + one D2H of that block into pinned h_out
-  float* h_out = nullptr;
-  cudaGraphExec_t graph_io = nullptr;
+  // graph_io[s] = the tick graph + one D2H of that block into pinned h_out[s];
+  // two slots let a caller submit tick t+1 before collecting tick t
+  float* h_out[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph_io[2] = {nullptr, nullptr};
+  cudaEvent_t io_done[2] = {nullptr, nullptr};
+  bool io_busy[2] = {false, false};
   std::vector<LayerPlan> plans;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
@@ -179,10 +185,13 @@ cudaStream_t pick(hb_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) 
 void free_selection(hb_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   c->graph = nullptr;
-  if (c->graph_io) cudaGraphExecDestroy(c->graph_io);
-  c->graph_io = nullptr;
-  if (c->h_out) cudaFreeHost(c->h_out);
-  c->h_out = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    if (c->graph_io[k]) cudaGraphExecDestroy(c->graph_io[k]);
+    c->graph_io[k] = nullptr;
+    if (c->h_out[k]) cudaFreeHost(c->h_out[k]);
+    c->h_out[k] = nullptr;
+    c->io_busy[k] = false;
+  }
   for (auto& a : c->act) cudaFree(a);
   c->act.clear();
   for (auto& g : c->groups) {
@@ -369,7 +378,7 @@ int build_selection(hb_ctx* c) {
   CK(c, cudaMalloc(&c->member_logits, sizeof(float) * out_floats));
   c->ens_prob = c->member_logits + static_cast<size_t>(c->P) * M;
   c->ens_logit = c->ens_prob + c->P;
-  CK(c, cudaHostAlloc(&c->h_out, sizeof(float) * out_floats, cudaHostAllocDefault));
+  for (int k = 0; k < 2; ++k) CK(c, cudaHostAlloc(&c->h_out[k], sizeof(float) * out_floats, cudaHostAllocDefault));
   CK(c, cudaMalloc(&c->ens_sums, sizeof(float) * 2 * c->P));
   std::vector<HeadMember> heads(M);
   for (auto& g : c->groups) {
@@ -472,11 +481,12 @@ int build_selection(hb_ctx* c) {
   CK(c, ec);
   CK(c, cudaGraphInstantiate(&c->graph, g, 0));
   cudaGraphDestroy(g);
-  {  // the same tick + one D2H of the output block into pinned h_out (hb_tick with host outputs)
+  for (int k = 0; k < 2; ++k) {  // the same tick reading staged_io[k] + one D2H of the outputs into h_out[k]
     cudaGraph_t gio;
+    c->staged = c->staged_io[k];
     CK(c, cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     const int rc2 = enqueue_tick(c, cap);
-    const cudaError_t e2 = rc2 == HB_OK ? cudaMemcpyAsync(c->h_out, c->member_logits, sizeof(float) * out_floats,
+    const cudaError_t e2 = rc2 == HB_OK ? cudaMemcpyAsync(c->h_out[k], c->member_logits, sizeof(float) * out_floats,
                                                            cudaMemcpyDeviceToHost, cap)
                                         : cudaSuccess;
     cudaError_t ec2 = cudaStreamEndCapture(cap, &gio);
@@ -486,9 +496,10 @@ int build_selection(hb_ctx* c) {
     }
     CK(c, e2);
     CK(c, ec2);
-    CK(c, cudaGraphInstantiate(&c->graph_io, gio, 0));
+    CK(c, cudaGraphInstantiate(&c->graph_io[k], gio, 0));
     cudaGraphDestroy(gio);
   }
+  c->staged = c->staged_io[0];
   cudaStreamDestroy(cap);
   c->dirty = false;
   return HB_OK;
@@ -535,12 +546,17 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   bool ok = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) == cudaSuccess &&
             cudaMalloc(&c->ring, S * c->R * sizeof(float)) == cudaSuccess &&
             cudaMemset(c->ring, 0, S * c->R * sizeof(float)) == cudaSuccess &&
-            cudaMalloc(&c->staged, S * c->hop * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->staged_io[0], S * c->hop * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->staged_io[1], S * c->hop * sizeof(float)) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->h2d_done[0], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->h2d_done[1], cudaEventDisableTiming) == cudaSuccess &&
             cudaMalloc(&c->prefill, S * c->R * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&c->wpos, sizeof(long long)) == cudaSuccess &&
             cudaMemset(c->wpos, 0, sizeof(long long)) == cudaSuccess &&
             cudaMalloc(&c->stats, S * 2 * sizeof(float)) == cudaSuccess &&
             cudaEventCreate(&c->t0) == cudaSuccess && cudaEventCreate(&c->t1) == cudaSuccess;
+  if (ok) c->staged = c->staged_io[0];
   if (ok && c->keep) ok = cudaMalloc(&c->raw, S * c->W * sizeof(float)) == cudaSuccess;
   if (!ok) {
     hb_destroy(c);
@@ -557,7 +573,11 @@ int hb_destroy(hb_ctx* c) {
   free_selection(c);
   for (auto& kv : c->members) free_member(kv.second);
   cudaFree(c->ring);
-  cudaFree(c->staged);
+  cudaFree(c->staged_io[0]);
+  cudaFree(c->staged_io[1]);
+  for (int k = 0; k < 2; ++k)
+    if (c->h2d_done[k]) cudaEventDestroy(c->h2d_done[k]);
+  if (c->copy) cudaStreamDestroy(c->copy);
   cudaFree(c->prefill);
   cudaFree(c->wpos);
   cudaFree(c->xn);
@@ -565,6 +585,8 @@ int hb_destroy(hb_ctx* c) {
   cudaFree(c->stats);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
+  for (int k = 0; k < 2; ++k)
+    if (c->io_done[k]) cudaEventDestroy(c->io_done[k]);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return HB_OK;
@@ -708,27 +730,83 @@ int hb_tick_device(hb_ctx* c, void* stream) {
   return HB_OK;
 }
 
+namespace {
+// overlap_h2d: the H2D runs on the copy stream into the slot's staging buffer
+// (pipelined submit); otherwise in-stream (blocking tick: lowest latency).
+int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool overlap_h2d);
+}  // namespace
+
+int hb_tick_submit(hb_ctx* c, const float* samples, int slot, void* stream) {
+  return tick_submit(c, samples, slot, stream, true);
+}
+
+namespace {
+int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool overlap_h2d) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  if (slot < 0 || slot > 1) return fail(c, HB_E_INVALID, "slot must be 0 or 1");
+  cudaSetDevice(c->device);
+  cudaStream_t st = pick(c, stream);
+  const int rc = build_selection(c);
+  if (rc) return rc;
+  if (c->io_busy[slot]) return fail(c, HB_E_STATE, "slot " + std::to_string(slot) + " has an uncollected tick");
+  if (samples && overlap_h2d) {  // H2D on the copy stream into this slot's staging buffer: overlaps the tick in flight
+    CK(c, cudaMemcpyAsync(c->staged_io[slot], samples, sizeof(float) * c->P * c->leads * c->hop,
+                          cudaMemcpyHostToDevice, c->copy));
+    CK(c, cudaEventRecord(c->h2d_done[slot], c->copy));
+    CK(c, cudaStreamWaitEvent(st, c->h2d_done[slot], 0));
+  } else if (samples) {
+    CK(c, cudaMemcpyAsync(c->staged_io[slot], samples, sizeof(float) * c->P * c->leads * c->hop,
+                          cudaMemcpyHostToDevice, st));
+  } else if (slot != 0) {
+    return fail(c, HB_E_INVALID, "samples staged with hb_stage_device are in slot 0");
+  }
+  CK(c, cudaEventRecord(c->t0, st));
+  CK(c, cudaGraphLaunch(c->graph_io[slot], st));
+  CK(c, cudaEventRecord(c->t1, st));
+  if (!c->io_done[slot]) CK(c, cudaEventCreateWithFlags(&c->io_done[slot], cudaEventDisableTiming));
+  CK(c, cudaEventRecord(c->io_done[slot], st));
+  c->timed = true;
+  c->io_busy[slot] = true;
+  return HB_OK;
+}
+
+}  // namespace
+
+int hb_tick_collect(hb_ctx* c, int slot, float* member_logits, float* ens_prob, float* ens_mean_logit) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  if (slot < 0 || slot > 1) return fail(c, HB_E_INVALID, "slot must be 0 or 1");
+  if (!c->io_busy[slot]) return fail(c, HB_E_STATE, "slot " + std::to_string(slot) + " has no submitted tick");
+  cudaSetDevice(c->device);
+  c->io_busy[slot] = false;
+  CK(c, cudaEventSynchronize(c->io_done[slot]));
+  const size_t P = c->P, M = c->selected.size();
+  const float* h = c->h_out[slot];
+  if (member_logits) std::memcpy(member_logits, h, sizeof(float) * P * M);
+  if (ens_prob) std::memcpy(ens_prob, h + P * M, sizeof(float) * P);
+  if (ens_mean_logit) std::memcpy(ens_mean_logit, h + P * M + P, sizeof(float) * P);
+  return HB_OK;
+}
+
 int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_prob, float* ens_mean_logit,
             void* stream) {
   if (!c) return fail(c, HB_E_INVALID, "null argument");
+  const bool host_out = member_logits || ens_prob || ens_mean_logit;
+  if (host_out) {
+    int slot = c->io_busy[0] ? (c->io_busy[1] ? -1 : 1) : 0;
+    if (slot < 0) return fail(c, HB_E_STATE, "both tick slots hold uncollected ticks");
+    const int rc = tick_submit(c, samples, slot, stream, false);
+    return rc ? rc : hb_tick_collect(c, slot, member_logits, ens_prob, ens_mean_logit);
+  }
   cudaSetDevice(c->device);
   cudaStream_t st = pick(c, stream);
   const int rc = build_selection(c);
   if (rc) return rc;
   if (samples)
     CK(c, cudaMemcpyAsync(c->staged, samples, sizeof(float) * c->P * c->leads * c->hop, cudaMemcpyHostToDevice, st));
-  const bool host_out = member_logits || ens_prob || ens_mean_logit;
   CK(c, cudaEventRecord(c->t0, st));
-  CK(c, cudaGraphLaunch(host_out ? c->graph_io : c->graph, st));
+  CK(c, cudaGraphLaunch(c->graph, st));
   CK(c, cudaEventRecord(c->t1, st));
   c->timed = true;
-  if (host_out) {
-    CK(c, cudaStreamSynchronize(st));
-    const size_t P = c->P, M = c->selected.size();
-    if (member_logits) std::memcpy(member_logits, c->h_out, sizeof(float) * P * M);
-    if (ens_prob) std::memcpy(ens_prob, c->h_out + P * M, sizeof(float) * P);
-    if (ens_mean_logit) std::memcpy(ens_mean_logit, c->h_out + P * M + P, sizeof(float) * P);
-  }
   return HB_OK;
 }
 

@@ -75,6 +75,9 @@ class EnsembleEngine:
         _lib.check(L.hb_create(device, C.byref(cfg), C.byref(h)))
         self._h = h
         self._hb_tick = L.hb_tick
+        self._hb_submit = L.hb_tick_submit
+        self._hb_collect = L.hb_tick_collect
+        self._next_slot = 0
         self._out_ptrs = None  # (out, member_logits, ens_prob, ens_mean_logit addresses) of the last TickResult
         self._registered: set = set()
         to_register = range(zoo.n) if register == "all" else selector.indices()
@@ -124,6 +127,13 @@ class EnsembleEngine:
         with self._lock:
             _lib.check(_lib.lib().hb_ingest(self._h, _lib.fptr(a), a.shape[2], None), self._h)
 
+    def _ptrs_of(self, out: TickResult) -> tuple:
+        for arr, shape in ((out.member_logits, (self.patients, self.selector.popcount)),
+                           (out.ens_prob, (self.patients,)), (out.ens_mean_logit, (self.patients,))):
+            if arr.dtype != np.float32 or not arr.flags.c_contiguous or arr.shape != shape:
+                raise ValueError(f"output buffers must be C-contiguous float32 of shape {shape}")
+        return (out, out.member_logits.ctypes.data, out.ens_prob.ctypes.data, out.ens_mean_logit.ctypes.data)
+
     def tick(self, samples, out: TickResult | None = None) -> TickResult:
         """Append one hop [P, leads, hop] and score every patient's latest window.
 
@@ -142,14 +152,42 @@ class EnsembleEngine:
                              np.empty(self.patients, np.float32), np.empty(self.patients, np.float32))
         cached = self._out_ptrs
         if cached is None or cached[0] is not out:
-            for arr, shape in ((out.member_logits, (self.patients, self.selector.popcount)),
-                               (out.ens_prob, (self.patients,)), (out.ens_mean_logit, (self.patients,))):
-                if arr.dtype != np.float32 or not arr.flags.c_contiguous or arr.shape != shape:
-                    raise ValueError(f"output buffers must be C-contiguous float32 of shape {shape}")
-            cached = self._out_ptrs = (out, out.member_logits.ctypes.data, out.ens_prob.ctypes.data,
-                                       out.ens_mean_logit.ctypes.data)
+            cached = self._out_ptrs = self._ptrs_of(out)
         with self._lock:
             rc = self._hb_tick(self._h, a.ctypes.data, cached[1], cached[2], cached[3], None)
+        if rc:
+            _lib.check(rc, self._h)
+        return out
+
+    def submit(self, samples) -> int:
+        """Pipelined tick, first half: enqueue the H2D of this hop, the tick and the D2H of its
+        outputs into one of two pinned slots, and return the slot without waiting.  Submit tick
+        t+1 before ``collect``-ing tick t and the device never idles on the host round trip.
+        Ticks run in submission order (one stream per engine)."""
+        if (type(samples) is np.ndarray and samples.dtype == np.float32 and samples.flags.c_contiguous
+                and samples.shape == (self.patients, self.leads, self.hop)):
+            a = samples
+        else:
+            a = self._check_block(samples, self.hop)
+        slot = self._next_slot
+        with self._lock:
+            rc = self._hb_submit(self._h, a.ctypes.data, slot, None)
+        if rc:
+            _lib.check(rc, self._h)
+        self._next_slot = slot ^ 1
+        return slot
+
+    def collect(self, slot: int, out: TickResult | None = None) -> TickResult:
+        """Pipelined tick, second half: wait for the tick submitted into ``slot`` and return its outputs."""
+        if out is None:
+            M = self.selector.popcount
+            out = TickResult(self.member_ids, np.empty((self.patients, M), np.float32),
+                             np.empty(self.patients, np.float32), np.empty(self.patients, np.float32))
+        cached = self._out_ptrs
+        if cached is None or cached[0] is not out:
+            cached = self._out_ptrs = self._ptrs_of(out)
+        with self._lock:
+            rc = self._hb_collect(self._h, slot, cached[1], cached[2], cached[3])
         if rc:
             _lib.check(rc, self._h)
         return out

@@ -143,3 +143,34 @@ def test_patient_chunking_is_bit_identical(monkeypatch):
             outs.append(eng.tick(streams[:, :, W:W + hop]))
     assert np.array_equal(outs[0].member_logits, outs[1].member_logits)
     assert np.array_equal(outs[0].ens_prob, outs[1].ens_prob)
+
+
+def test_pipelined_submit_collect_matches_blocking_ticks():
+    """submit(t+1) before collect(t): same outputs, bit for bit, as one blocking tick per step;
+    a third submit while both slots hold uncollected ticks is refused."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [0, 21])
+    P, W, hop, n = 4, 7500, 250, 6
+    streams = _streams(P, W + n * hop, seed=3)
+    blocks = [np.ascontiguousarray(streams[:, :, W - hop + k * hop: W + k * hop]) for k in range(n)]
+    ref = []
+    with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        for b in blocks:
+            r = eng.tick(b)
+            ref.append((r.member_logits.copy(), r.ens_prob.copy(), r.ens_mean_logit.copy()))
+    got = []
+    with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        slot = eng.submit(blocks[0])
+        for k in range(n):
+            nxt = eng.submit(blocks[k + 1]) if k + 1 < n else None
+            if k == 0:
+                with pytest.raises(RuntimeError):
+                    eng.submit(blocks[0])   # both slots busy (HB_E_STATE)
+            r = eng.collect(slot)
+            got.append((r.member_logits.copy(), r.ens_prob.copy(), r.ens_mean_logit.copy()))
+            slot = nxt
+    for (a, b, c), (x, y, z) in zip(ref, got):
+        assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
