@@ -120,6 +120,7 @@ struct hb_ctx {
   int device = 0, P = 0, leads = 0, fs = 0, W = 0, hop = 0, R = 0, keep = 0, num_sms = 148;
   int max_lanes = 4;  // concurrent member branches in the tick graph (HB_LANES overrides)
   int group_off = 0;  // HB_NO_GROUP=1: one launch per member and layer (A/B experiments)
+  int max_group = kMaxGroup;  // HB_MAX_GROUP: cap on members per grouped launch (A/B experiments)
   // patient micro-batching: member chains run over chunks of Pc beds so the
   // activation buffers stay within act_budget (the rings / windows hold all P)
   int Pc = 0, n_chunks = 1, P_pad = 0;
@@ -315,7 +316,7 @@ int build_selection(hb_ctx* c) {
     Group* gp = nullptr;
     if (!c->group_off)
       for (auto& g : c->groups)
-        if (g.width == m.width && g.depth == m.depth && static_cast<int>(g.mi.size()) < kMaxGroup) gp = &g;
+        if (g.width == m.width && g.depth == m.depth && static_cast<int>(g.mi.size()) < c->max_group) gp = &g;
     if (!gp) {
       c->groups.emplace_back();
       gp = &c->groups.back();
@@ -536,6 +537,7 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   c->keep = cfg->keep_windows;
   if (getenv("HB_LANES")) c->max_lanes = std::max(1, atoi(getenv("HB_LANES")));
   if (getenv("HB_NO_GROUP")) c->group_off = atoi(getenv("HB_NO_GROUP"));
+  if (getenv("HB_MAX_GROUP")) c->max_group = std::max(1, std::min(kMaxGroup, atoi(getenv("HB_MAX_GROUP"))));
   if (getenv("HB_ACT_BUDGET_GB")) c->act_budget = atof(getenv("HB_ACT_BUDGET_GB")) * 1e9;
   if (c->R < c->W) {
     delete c;
