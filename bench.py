@@ -199,10 +199,21 @@ def tick_at(zoo, sel, P, hop, device, K=30, warm=5):
     torch.cuda.synchronize()
     t = [a.elapsed_time(b) for a, b in ms]
     flops, _ = eng.tick_work()
+    # the memory-bound stream kernels at this scale: achieved HBM GB/s of ingest+window
+    # (algorithmic bytes: append 8 B + window 4 B read + 2 B write per sample) and aggregate
+    kinds, kms, _, kbytes = eng.profile_tick(st.cuda_stream)
+    torch.cuda.synchronize()
+    stream_k = {}
+    for kind, name in ((0, "ingest_window"), (3, "aggregate")):
+        sel_k = kinds == kind
+        if sel_k.any():
+            tms = float(kms[sel_k].sum())
+            stream_k[name] = {"ms": tms, "bytes": float(kbytes[sel_k].sum()),
+                              "gbs": float(kbytes[sel_k].sum()) / (tms / 1e3) / 1e9 if tms > 0 else None}
     eng.close()
     return {"patients": P, "tick_ms_p50": pct(t, 50), "tick_ms_p99": pct(t, 99),
             "patient_windows_per_s": P / (float(np.mean(t)) / 1e3),
-            "tflops": flops / (float(np.mean(t)) / 1e3) / 1e12, "ticks": K}
+            "tflops": flops / (float(np.mean(t)) / 1e3) / 1e12, "ticks": K, "stream_kernels_eager": stream_k}
 
 
 def sweep_bench(device):
@@ -349,6 +360,13 @@ def run_b200(args):
     tick_ms_eager = float(ms.sum())
     achieved = pp_flops / (pp_ms / 1e3) / 1e12 if pp_ms > 0 else conv_flops / (conv_ms / 1e3) / 1e12
     peak_tf, peak_hbm, peak_src = peaks()
+    # K4b against its own per-launch roofline: sum over its launches of
+    # max(FLOPs / tensor peak, algorithmic activation bytes / HBM peak), over the measured time
+    abytes = prof[0][3]
+    pp_roof_ms = float(sum(max(flops[i] / (peak_tf * 1e12), abytes[i] / (peak_hbm * 1e9)) * 1e3
+                           for i in range(len(kinds)) if kinds[i] == 5))
+    pp_hbm_bound = int(sum(1 for i in range(len(kinds))
+                           if kinds[i] == 5 and abytes[i] / (peak_hbm * 1e9) > flops[i] / (peak_tf * 1e12)))
     traffic, ncu_meta = ncu_traffic()
     n_launch = int(len(kinds))
 
@@ -414,6 +432,10 @@ def run_b200(args):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic, "kernel": "hb::conv_pp_kernel (K4b)",
                      "launches_per_tick": pp_n, "share_of_tick": pp_ms / tick_ms_eager, "peak_source": peak_src,
+                     "time_roofline": {"frac": pp_roof_ms / pp_ms if pp_ms > 0 else None, "roofline_ms": pp_roof_ms,
+                                       "measured_ms": pp_ms, "hbm_bound_launches": pp_hbm_bound,
+                                       "def": "sum over K4b launches of max(FLOPs/tensor peak, activation bytes/HBM peak) "
+                                              "/ their measured eager ms"},
                      "achieved_def": "sum K4b algorithmic FLOPs / sum K4b launch ms over one tick "
                                      "(2*Cin*Cout*16*Lout*P per layer; the zero taps K4b also issues are not counted)",
                      "all_conv": {"kernels": "K4b + K4 (hb::conv_tc_kernel)", "tflops": conv_flops / (conv_ms / 1e3) / 1e12,

@@ -301,7 +301,12 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   }
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
                          c->ens_logit, c->ens_sums, c->wpos, c->hop, st));
-  pr->mark(st, K_AGG, 0.0, 0.0);  // (the cursor advance, K_ADV, is fused into the aggregate)
+  {  // algorithmic bytes: every member's head partials in, member logits + 2 ensemble outputs + 2 sums out
+    double partials = 0.0;
+    for (const Group& g : c->groups) partials += static_cast<double>(g.mi.size()) * g.head_mt;
+    const double M = static_cast<double>(c->selected.size());
+    pr->mark(st, K_AGG, 0.0, P * 4.0 * (partials + M + 4.0));  // (the cursor advance, K_ADV, is fused in)
+  }
   return HB_OK;
 }
 
