@@ -453,16 +453,27 @@ int build_selection(hb_ctx* c) {
         float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
         LayerPlan plan;
         plan.kind = g.kind[li];
+        // HB_LANE_SMS="a,b,..": cap the grid of lane k's conv launches (SM partition experiment)
+        int lane_sms = c->num_sms;
+        if (const char* ls = getenv("HB_LANE_SMS")) {
+          int k = 0;
+          for (const char* q = ls; *q; ++k) {
+            const int v = atoi(q);
+            if (k == g.lane && v > 0) lane_sms = std::min(v, c->num_sms);
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+          }
+        }
         const char* e;
         if (plan.kind == KIND_PP) {
           e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src], act[dst], out_q,
                       g.wpack[li - 1], g.bias[li - 1], res, conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q,
-                      c->num_sms, layer_zc(L));
+                      lane_sms, layer_zc(L));
         } else {
           e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
                         L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
                         conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, L.head ? g.fc_w : nullptr, head_base,
-                        c->num_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
+                        lane_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
           if (!e && L.head && plan.tc.args.n_ntiles * plan.tc.args.mt_per_p != g.head_mt) e = "head tiling mismatch";
         }
         if (e) return fail(c, HB_E_INVALID, e);
