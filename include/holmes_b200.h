@@ -198,6 +198,8 @@ int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const fl
                    int cout, const void* res, int res_mode, int res_c, int res_len, int res_q, void* out, int out_q,
                    const float* fc_w_host, float* head_out, int kind, void* stream);
 int hb_conv_kind(int cin, int cout, int stride, int head);
+/* Head partials per patient (head_out of hb_op_conv1d_q is [P][this]) for a head layer of `kind`. */
+int hb_conv_head_mt(int P, int cin, int cout, int lin, int stride, int res_mode, int kind);
 /* M tiles per patient of a conv layer (head_out of hb_op_conv1d is [P][this]). */
 int hb_conv_mt(int cin, int cout, int lin, int stride, int head);
 /* Micro-benchmark of one conv layer shape on zero data: mean ms per launch. */

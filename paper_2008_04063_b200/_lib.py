@@ -79,6 +79,7 @@ _SIGS = {
     "hb_op_conv1d_q": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, C.c_int,
                                  C.c_int, C.c_int, _P, C.c_int, _F, _P, C.c_int, _P]),
     "hb_conv_kind": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "hb_conv_head_mt": (C.c_int, [C.c_int] * 7),
     "hb_bench_conv_k": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
     "hb_op_stem_q": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, _P]),
 }

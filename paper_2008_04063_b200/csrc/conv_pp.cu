@@ -331,6 +331,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       const size_t out_plane = static_cast<size_t>(t.p) * out_groups + g8;
       const size_t res_plane = static_cast<size_t>(t.p) * res_groups + g8;
       const int n_base = t.nt * a.nb + r8;  // + 16*ch + 8*b: this lane's column after the transpose
+      float head = 0.f;
+      float fc8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) fc8[k] = a.fc_w ? a.fc_w[static_cast<size_t>(t.g) * a.cout + g8 * 8 + k] : 0.f;
       // Shortcut rows of a chunk (2 positions per lane after the transpose;
       // maxpool reads 2 rows each) are loaded one chunk ahead, the first
       // before the accumulator wait.
@@ -410,9 +414,24 @@ __global__ void __launch_bounds__(kPPThreads, 1)
               const __half2 y = __hmax2(__hadd2(*reinterpret_cast<const __half2*>(&h[k]), rr[k]), zero);
               o2[k] = valid ? y : zero;
             }
-            *reinterpret_cast<uint4*>(a.out + q_off(out_plane, a.out_qs, a.out_lq, l)) = pk;
+            if (a.fc_w == nullptr) {
+              *reinterpret_cast<uint4*>(a.out + q_off(out_plane, a.out_qs, a.out_lq, l)) = pk;
+            } else if (valid) {  // fused head: this position's 8 channels . fc
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(o2[k]);
+                head = fmaf(f.x, fc8[2 * k], fmaf(f.y, fc8[2 * k + 1], head));
+              }
+            }
           }
         }
+      }
+      if (a.fc_w != nullptr) {  // one partial per (tile, epilogue warp), summed in fixed order by K5
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) head += __shfl_xor_sync(0xffffffffu, head, off);
+        if (lane == 0)
+          a.head_out[static_cast<size_t>(t.g) * a.head_g_stride + static_cast<size_t>(t.p - t.g * a.Pm) * a.head_mt +
+                     static_cast<size_t>(t.nt) * 8 + (ew >> 1) * 4 + wq] = head;  // (column half, warp)
       }
       if (eprof) e_work += clock64() - e0;
       accph ^= 1u;
@@ -530,7 +549,8 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const int* f
 
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
-                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc) {
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc,
+                    const float* fc_w, float* head_out, size_t head_g_stride) {
   std::memset(plan, 0, sizeof(*plan));
   if (G < 1 || G > kMaxGroup || Pm < 1) return "conv_pp: bad group shape";
   if (!pp_shape_ok(cin, cout, stride)) return "conv_pp: unsupported layer shape";
@@ -601,6 +621,10 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   a.bias = bias;
   a.bias_stride = static_cast<int>(bias_len(cout));
   a.out = out;
+  a.fc_w = fc_w;
+  a.head_out = head_out;
+  a.head_mt = a.nt_per_p * 8;
+  a.head_g_stride = head_g_stride ? head_g_stride : static_cast<size_t>(Pm) * a.head_mt;
   a.res = res;
   a.res_mode = (res && !res_mma) ? res_mode : 0;  // the epilogue's share of the shortcut
   a.res_c = res ? res_c : 0;

@@ -56,7 +56,20 @@ std::vector<LayerSpec> member_layers(int width, int depth, int window) {
 // graph sending every supported layer to K4b is fastest (c2 0.947 vs 0.958 ms
 // with a size rule, profiles/r01_pp_ab.txt).  HB_PP=0 keeps every layer on K4.
 enum { KIND_TC = 0, KIND_PP = 1 };
-bool pp_eligible(const LayerSpec& L) { return !L.head && L.cin >= 16 && pp_shape_ok(L.cin, L.cout, L.stride); }
+bool pp_eligible(const LayerSpec& L) {
+  static const bool heads = !(getenv("HB_PP_HEAD") && atoi(getenv("HB_PP_HEAD")) == 0);
+  return (heads || !L.head) && L.cin >= 16 && pp_shape_ok(L.cin, L.cout, L.stride);
+}
+// Head partials per patient of a K4b head layer (nt_per_p * 8), from a dry-run plan.
+int pp_head_mt(const LayerSpec& L, int G, int Pm, int sms) {
+  PPPlan plan;
+  __half* fake = reinterpret_cast<__half*>(static_cast<uintptr_t>(1) << 20);  // encoded, never dereferenced
+  const char* e = plan_pp(&plan, G, Pm, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, fake, nullptr, 1,
+                          reinterpret_cast<uint8_t*>(fake), nullptr, L.res_mode ? fake : nullptr, L.res_mode, L.res_c,
+                          L.res_mode == 2 ? 2 * L.lout : L.lout, L.res_mode == 2 ? 2 : 1, sms, 0,
+                          reinterpret_cast<const float*>(fake), reinterpret_cast<float*>(fake), 0);
+  return e ? -1 : plan.args.head_mt;
+}
 int layer_kind(const LayerSpec& L) {
   static const int pp_on = getenv("HB_PP") ? atoi(getenv("HB_PP")) : 1;
   return (pp_on && pp_eligible(L)) ? KIND_PP : KIND_TC;
@@ -409,10 +422,15 @@ int build_selection(hb_ctx* c) {
       g.bias.push_back(b);
     }
     CK(c, cudaMalloc(&g.fc_w, sizeof(float) * c_last * G));
-    {  // head partials per (patient, N tile, M tile) of the last layer, as that layer is tiled
+    {  // head partials per patient of the last layer, as that layer is tiled
       const LayerSpec& H = g.layers.back();
-      const int bn = conv_bn(H.cout), sm = conv_stride_m(conv_fold(H.cin, H.cout, H.stride));
-      g.head_mt = ((round_up(H.cout, 16) + bn - 1) / bn) * ((H.lout + sm - 1) / sm);
+      if (g.kind.back() == KIND_PP) {
+        g.head_mt = pp_head_mt(H, G, c->Pc, c->num_sms);
+        if (g.head_mt <= 0) return fail(c, HB_E_INVALID, "conv_pp: head layer does not plan");
+      } else {
+        const int bn = conv_bn(H.cout), sm = conv_stride_m(conv_fold(H.cin, H.cout, H.stride));
+        g.head_mt = ((round_up(H.cout, 16) + bn - 1) / bn) * ((H.lout + sm - 1) / sm);
+      }
     }
     CK(c, cudaMalloc(&g.head_partial, sizeof(float) * G * c->P_pad * g.head_mt));
     g.stem.assign(c->n_chunks, {});
@@ -466,9 +484,11 @@ int build_selection(hb_ctx* c) {
         }
         const char* e;
         if (plan.kind == KIND_PP) {
-          e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src], act[dst], out_q,
-                      g.wpack[li - 1], g.bias[li - 1], res, conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q,
-                      lane_sms, layer_zc(L));
+          e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
+                      L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
+                      conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, lane_sms, layer_zc(L),
+                      L.head ? g.fc_w : nullptr, head_base, static_cast<size_t>(c->P_pad) * g.head_mt);
+          if (!e && L.head && plan.pp.args.head_mt != g.head_mt) e = "conv_pp: head tiling mismatch";
         } else {
           e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
                         L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
@@ -955,7 +975,6 @@ int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const fl
   const int tot = (lout - 1) * stride + kTaps - lin;
   const int pad = tot > 0 ? tot / 2 : 0;
   if (kind < 0) kind = layer_kind({cin, cout, stride, lin, lout, pad, res_mode, res_c, fc_w_host ? 1 : 0});
-  if (kind == KIND_PP && fc_w_host) return fail(nullptr, HB_E_INVALID, "conv_pp: no fused head");
   const LayerSpec spec{cin, cout, stride, lin, lout, pad, res_mode, res_c, fc_w_host ? 1 : 0};
   const size_t wb = layer_wbytes(spec, kind);
   std::vector<uint16_t> img(wb / 2);
@@ -980,7 +999,7 @@ int hb_op_conv1d_q(const void* in, int P, int cin, int lin, int stride, const fl
   if (kind == KIND_PP)
     e = plan_pp(&plan.pp, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
                 static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
-                res_len > 0 ? res_len : lout, res_q, sms, layer_zc(spec));
+                res_len > 0 ? res_len : lout, res_q, sms, layer_zc(spec), dfc, head_out, 0);
   else
     e = plan_conv(&plan.tc, 1, P, cin, cout, lin, lout, stride, pad, static_cast<const __half*>(in),
                   static_cast<__half*>(out), out_q, dw, db, static_cast<const __half*>(res), res_mode, res_c,
@@ -1008,6 +1027,20 @@ int hb_op_conv1d(const void* in, int P, int cin, int lin, int stride, const floa
                  const float* fc_w_host, float* head_out, void* stream) {
   return hb_op_conv1d_q(in, P, cin, lin, stride, w_host, b_host, cout, res, res_mode, res_c, res_len,
                         res_mode == 2 ? 2 : 1, out, out_split ? 2 : 1, fc_w_host, head_out, KIND_TC, stream);
+}
+
+int hb_conv_head_mt(int P, int cin, int cout, int lin, int stride, int res_mode, int kind) {
+  const int lout = (lin + stride - 1) / stride;
+  const int tot = (lout - 1) * stride + kTaps - lin;
+  const LayerSpec L{cin, cout, stride, lin, lout, tot > 0 ? tot / 2 : 0, res_mode, cin < cout ? cin : cout, 1};
+  if (kind < 0) kind = layer_kind(L);
+  if (kind == KIND_PP) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return pp_head_mt(L, 1, P, sms);
+  }
+  return hb_conv_mt(cin, cout, lin, stride, 1);
 }
 
 int hb_conv_kind(int cin, int cout, int stride, int head) {

@@ -110,6 +110,10 @@ struct PPArgs {
   int out_qs, out_lq, out_rows;
   const __half* res;
   int res_mode, res_c, res_qs, res_lq;
+  const float* fc_w;               // fused mean-pool.FC head ([G][cout]) instead of an output, or null
+  float* head_out;                 // [G][head_g_stride]: per patient head_mt = nt_per_p*8 partials
+  size_t head_g_stride;
+  int head_mt;
   int dbg;                         // experiments only (HB_PP_DBG): 1 no epilogue math/stores, 2 no MMAs, 4 no B loads,
                                    // 8 no shortcut L2 prefetch, 16 role cycle counters into prof
   unsigned long long* prof;        // dbg & 16: per CTA [8]
@@ -129,7 +133,8 @@ size_t pp_wbytes(int cin, int cout, int stride, int zc = 0);
 void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst /* fp16 bits */, int zc = 0);
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
-                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc = 0);
+                    const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc = 0,
+                    const float* fc_w = nullptr, float* head_out = nullptr, size_t head_g_stride = 0);
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
 cudaError_t init_pp_kernel();
 

@@ -151,5 +151,39 @@ def test_planner_routes_narrow_layers_to_pp():
     assert L.lib().hb_conv_kind(32, 32, 1, 0) == K_PP
     assert L.lib().hb_conv_kind(32, 32, 2, 0) == K_PP
     assert L.lib().hb_conv_kind(128, 128, 1, 0) == K_TC
-    assert L.lib().hb_conv_kind(32, 32, 1, 1) == K_TC   # fused head stays on K4
+    assert L.lib().hb_conv_kind(32, 32, 1, 1) == K_PP   # fused head on K4b too
+    assert L.lib().hb_conv_kind(128, 128, 1, 1) == K_TC
     assert L.lib().hb_conv_kind(8, 8, 1, 0) == K_TC
+
+
+@pytest.mark.parametrize("c,lin,P", [(64, 469, 3), (64, 1875, 2), (32, 938, 2), (16, 235, 4)])
+def test_pp_fused_head(c, lin, P):
+    """Last conv of a member on K4b: maxpool shortcut + ReLU + mean-pool.FC fused into the epilogue;
+    the per-(tile, warp) partials sum to the fp32 reference (fp16 activations inside the dot)."""
+    L = _lib()
+    g = torch.Generator().manual_seed(c + lin + 11)
+    x = torch.relu(_rand((P, c, lin), g))
+    blk = torch.relu(_rand((P, c, 2 * lin), g))
+    w = _rand((c, c, 16), g, (2.0 / (c * 16)) ** 0.5)
+    b = _rand((c,), g, 0.1)
+    fc = torch.randn(c, generator=g) / c ** 0.5
+    dev = torch.device("cuda")
+    in_q = 128 // c
+    res_q = 2
+    xin = to_q(x.to(dev), in_q)
+    rin = to_q(blk.to(dev), res_q)
+    mt = L.lib().hb_conv_head_mt(P, c, c, lin, 1, 2, K_PP)
+    assert mt > 0
+    head = torch.full((P, mt), 123.0, dtype=torch.float32, device=dev)
+    wn = np.ascontiguousarray(w.numpy(), np.float32)
+    bn = np.ascontiguousarray(b.numpy(), np.float32)
+    fcn = np.ascontiguousarray(fc.numpy(), np.float32)
+    L.check(L.lib().hb_op_conv1d_q(
+        C.c_void_p(xin.data_ptr()), P, c, lin, 1, L.fptr(wn), L.fptr(bn), c, C.c_void_p(rin.data_ptr()), 2, c,
+        2 * lin, res_q, None, 1, L.fptr(fcn), C.c_void_p(head.data_ptr()), K_PP,
+        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    ref = ref_conv(x, w, b, 1, blk, 2)
+    ref_sum = (ref * fc[None, :, None]).sum(dim=(1, 2))
+    got = head.cpu().sum(dim=1)
+    assert torch.allclose(got, ref_sum, rtol=2e-3, atol=2e-2), (got, ref_sum)
