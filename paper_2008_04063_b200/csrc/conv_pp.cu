@@ -195,25 +195,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             sph ^= 1u;
           }
         }
-        // The epilogue's shortcut reads are plain loads with little in
-        // flight; pull this tile's shortcut rows into L2 now (the tile is
-        // ~2 tiles ahead of its epilogue) so they hit L2.
-        if (a.res_mode && !(a.dbg & 8)) {
-          const int sc = a.res_mode == 2 ? 2 : 1;
-          const int pos_lo = sc * a.ph * t.nt * a.nb;
-          int pos_hi = sc * a.ph * (t.nt + 1) * a.nb;
-          const int res_rows = (1 << a.res_qs) * a.res_lq;
-          if (pos_hi > res_rows) pos_hi = res_rows;
-          const int r_lo = pos_lo >> a.res_qs, r_hi = min(a.res_lq, ((pos_hi - 1) >> a.res_qs) + 1);
-          if (r_hi > r_lo) {
-            const uint32_t bytes = static_cast<uint32_t>(r_hi - r_lo) * 16u;
-            for (int g = 0; g < a.res_c / 8; ++g)
-              for (int q = 0; q < (1 << a.res_qs); ++q) {
-                const size_t plane = static_cast<size_t>(t.p) * (a.res_c / 8) + g;
-                bulk_prefetch_l2(a.res + (((plane << a.res_qs) + q) * a.res_lq + r_lo) * 8, bytes);
-              }
-          }
-        }
       }
     }
   } else if (warp == 1) {

@@ -115,7 +115,7 @@ struct PPArgs {
   size_t head_g_stride;
   int head_mt;
   int dbg;                         // experiments only (HB_PP_DBG): 1 no epilogue math/stores, 2 no MMAs, 4 no B loads,
-                                   // 8 no shortcut L2 prefetch, 16 role cycle counters into prof
+                                   // 16 role cycle counters into prof, 32 zero shortcut rows, 64 L2-only shortcut loads
   unsigned long long* prof;        // dbg & 16: per CTA [8]
 };
 struct PPPlan {
