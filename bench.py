@@ -236,6 +236,20 @@ def sweep_bench(device):
         S = (1 << n) - 1
         out[f"n{n}"] = {"candidates": S, "N": 20000, "seconds": dt, "candidates_per_s": S / dt,
                         "best_auc_selector": format(best, f"0{n}b")[::-1], "best_auc": float(aucs[best - 1])}
+    # the recording leg of the profiler (north star (4)): every member of the n=10 zoo over
+    # N=20000 recorded windows on the serving kernels (tumbling, 1024 windows per device tick)
+    z = generate_zoo(1, [8, 16, 32, 64, 128], [2, 4], seed=3)
+    rng = np.random.default_rng(5)
+    wins = (rng.standard_normal((20000, 1, 7500)) * 0.3).astype(np.float32)
+    labels = (rng.random(20000) < 0.5).astype(np.int8)
+    hc.record_cohort(z, wins[:2048], labels[:2048], batch=1024, device=device)  # warm (build + graph)
+    t0 = time.perf_counter()
+    hc.record_cohort(z, wins, labels, batch=1024, device=device)
+    dt = time.perf_counter() - t0
+    out["record"] = {"windows": 20000, "members": z.n, "seconds": dt, "windows_per_s": 20000 / dt,
+                     "member_windows_per_s": 20000 * z.n / dt,
+                     "def": "cohort.record_cohort: host windows -> device -> every member's forward -> logits "
+                            "(includes engine setup; 1024 windows per tick, pipelined submit/collect)"}
     # CPU oracle (same algorithm, numpy, 1 core) on a bounded sample of the n=10 sweep
     z = generate_zoo(1, [8, 16, 32, 64, 128], [2, 4], seed=3)
     coh = hc.synthesize_cohort(z, 10000, 10000, 0.5, 0)

@@ -201,7 +201,7 @@ def accuracy_profile(cohort: Cohort, b: Selector, device: int = 0) -> AccuracyRe
 
 
 def record_cohort(zoo: ModelZoo, windows: np.ndarray, labels, *, selector: Selector | None = None, seed: int = 0,
-                  batch: int = 256, device: int = 0) -> Cohort:
+                  batch: int = 1024, device: int = 0) -> Cohort:
     """Member logits over recorded windows -> Cohort (north star (4)).
 
     windows: [N, leads, W] raw samples (one recorded window per row, every
@@ -218,13 +218,23 @@ def record_cohort(zoo: ModelZoo, windows: np.ndarray, labels, *, selector: Selec
     sel = selector if selector is not None else Selector.ones(zoo.n)
     P = max(1, min(batch, N))
     out = np.empty((N, sel.popcount))
+    starts = list(range(0, N, P))
+
+    def block(r0):
+        chunk = win[r0:r0 + P]
+        if chunk.shape[0] < P:
+            chunk = np.concatenate([chunk, np.zeros((P - chunk.shape[0], leads, W), np.float32)])
+        return np.ascontiguousarray(chunk)
+
     with EnsembleEngine(zoo, sel, P, leads=leads, fs=1, window_s=float(W), hop=W, seed=seed,
                         device=device) as eng:
-        for r0 in range(0, N, P):
-            chunk = win[r0:r0 + P]
-            if chunk.shape[0] < P:
-                chunk = np.concatenate([chunk, np.zeros((P - chunk.shape[0], leads, W), np.float32)])
-            res = eng.tick(chunk)
+        # pipelined: batch i+1 is submitted (copy + forward enqueued) before batch i is collected
+        pending = [(starts[0], eng.submit(block(starts[0])))]
+        for i in range(len(starts)):
+            if i + 1 < len(starts):
+                pending.append((starts[i + 1], eng.submit(block(starts[i + 1]))))
+            r0, slot = pending.pop(0)
+            res = eng.collect(slot)
             k = min(P, N - r0)
             out[r0:r0 + k] = res.member_logits[:k]
     return Cohort(labels=np.asarray(labels, np.int8), scores=out, seed=seed)
