@@ -36,10 +36,19 @@
 //
 // Roles (640 threads, 1 CTA/SM, persistent over tiles): warp 0 TMA producer,
 // warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-19 four epilogue
-// warpgroups (two per TMEM accumulator, one per half of its columns).  Epilogue thread r holds M
-// row r = (p', c) for nb columns; an 8x8 register transpose by warp shuffles
-// inside each 8-lane group turns that into 8 channels x one position per
-// lane, so the shortcut read and the output store are 16-byte rows.
+// warpgroups (two per TMEM accumulator, one per half of its columns).
+// Epilogue thread r holds M row r = (p', c) for nb columns; an 8x8 register
+// transpose by warp shuffles inside each 8-lane group turns that into 8
+// channels x one position per lane, so the shortcut read and the output store
+// are 16-byte rows.
+//
+// Shortcuts: an identity shortcut whose x is in this conv's own Q-phase
+// layout (ph >= 4) is added by the tensor core -- x's tile arrives as extra
+// B stages (second tensor map) and ph MMAs per 16 channels with A = a window
+// of a ones-array (appended to the weight image) add x[c, ph*n + p] to
+// D[(p', c), n].  Other shortcuts (maxpool, wider phases) are read by the
+// epilogue.  A member's last conv writes no output: the epilogue folds
+// mean-pool . FC into one partial per (tile, column half, warp).
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
