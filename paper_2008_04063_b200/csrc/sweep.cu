@@ -33,6 +33,7 @@
 #include "hb_kernels.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -235,6 +236,173 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_auc_kernel(const Sweep
   }
 }
 
+// ---------------------------------------------------------------------------
+// Radix variant (m <= kRadixMax): the smaller class is sorted by an LSD radix
+// sort in shared memory (8-bit digits, passes over constant bytes skipped),
+// stable per pass: each warp owns a contiguous block of keys and ranks equal
+// digits with __match_any_sync in lane order; offsets = exclusive scan over
+// (digit, warp).  No power-of-two padding, ~6-8 passes instead of 105 bitonic
+// stages.  Everything else (keys, exact rank statistic) is as above.
+constexpr int kRadixMax = 12288;                       // keys: 2 x 96 KB + counters
+constexpr int kRadixRounds = kRadixMax / kSweepThreads;  // keys per lane
+
+__device__ __forceinline__ unsigned long long* radix_sort_block(unsigned long long* a, unsigned long long* b, int m,
+                                                                unsigned* cnt, unsigned* base,
+                                                                unsigned long long diff) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int per_warp = (m + 31) / 32;
+  const int w0 = warp * per_warp;
+  const int w1 = min(m, w0 + per_warp);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int shift = 0; shift < 64; shift += 8) {
+    if (((diff >> shift) & 0xFFull) == 0) continue;  // every key has the same byte here
+    for (int i = tid; i < 32 * 256; i += kSweepThreads) cnt[i] = 0;
+    __syncthreads();
+    unsigned rank[kRadixRounds];
+#pragma unroll
+    for (int r = 0; r < kRadixRounds; ++r) {
+      const int i = w0 + r * 32 + lane;
+      const bool ok = i < w1;
+      const int d = ok ? static_cast<int>((a[i] >> shift) & 0xFFull) : 256 + lane;
+      const unsigned mm = __match_any_sync(0xffffffffu, d);
+      const unsigned before = ok ? cnt[warp * 256 + d] : 0u;
+      rank[r] = before + __popc(mm & lt);
+      __syncwarp();
+      if (ok && (mm & lt) == 0) cnt[warp * 256 + d] = before + __popc(mm);  // the group's first lane
+      __syncwarp();
+    }
+    __syncthreads();
+    if (tid < 256) {  // per digit: exclusive prefix over warps (in place), total -> base
+      unsigned run = 0;
+      for (int w = 0; w < 32; ++w) {
+        const unsigned c = cnt[w * 256 + tid];
+        cnt[w * 256 + tid] = run;
+        run += c;
+      }
+      base[tid] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 256 digit totals (8 per lane)
+      unsigned v[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        v[k] = base[lane * 8 + k];
+        sum += v[k];
+      }
+      unsigned incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      unsigned run = incl - sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        base[lane * 8 + k] = run;
+        run += v[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRadixRounds; ++r) {
+      const int i = w0 + r * 32 + lane;
+      if (i < w1) {  // (the key is re-read from smem: registers are capped at 64 per thread here)
+        const unsigned long long k = a[i];
+        const int d = static_cast<int>((k >> shift) & 0xFFull);
+        b[base[d] + cnt[warp * 256 + d] + rank[r]] = k;
+      }
+    }
+    __syncthreads();
+    unsigned long long* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+__global__ void __launch_bounds__(kSweepThreads, 1) sweep_auc_radix_kernel(const SweepArgs a) {
+  extern __shared__ __align__(16) unsigned long long s_ra[];  // [2][m] keys, then counters
+  unsigned long long* ka = s_ra;
+  unsigned long long* kb = s_ra + a.m;
+  unsigned* cnt = reinterpret_cast<unsigned*>(s_ra + 2 * a.m);  // [32][256]
+  unsigned* base = cnt + 32 * 256;                               // [256]
+  __shared__ int s_cols[kMaxCols];
+  __shared__ int s_pop;
+  __shared__ unsigned long long s_red[32];
+  const int tid = threadIdx.x;
+  for (long long s = blockIdx.x; s < a.S; s += gridDim.x) {
+    __syncthreads();
+    if (tid == 0) {
+      int pop = 0;
+      if (a.bits) {
+        const uint8_t* row = a.bits + static_cast<size_t>(s) * a.n;
+        for (int k = 0; k < a.n; ++k)
+          if (row[k]) s_cols[pop++] = k;
+      } else {
+        const unsigned long long v = a.first + static_cast<unsigned long long>(s);
+        for (int k = 0; k < a.n; ++k)
+          if ((v >> k) & 1ull) s_cols[pop++] = k;
+      }
+      s_pop = pop;
+    }
+    __syncthreads();
+    const int pop = s_pop;
+    const double dpop = static_cast<double>(pop);
+    for (int j = tid; j < a.m; j += kSweepThreads) {
+      double acc = 0.0;
+      for (int c = 0; c < pop; ++c) acc = acc + a.cols[static_cast<size_t>(s_cols[c]) * a.N + j];
+      const double mean = acc / dpop;
+      if (a.ens_out && s == 0) a.ens_out[j] = mean;
+      ka[j] = order_key(mean);
+    }
+    __syncthreads();
+    // bytes that differ between keys (passes over the others are no-ops)
+    unsigned long long diff = 0;
+    const unsigned long long k0 = ka[0];
+    for (int j = tid; j < a.m; j += kSweepThreads) diff |= ka[j] ^ k0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, off);
+    if ((tid & 31) == 0) s_red[tid >> 5] = diff;
+    __syncthreads();
+    diff = 0;
+#pragma unroll
+    for (int w = 0; w < kSweepThreads / 32; ++w) diff |= s_red[w];
+    __syncthreads();
+    const unsigned long long* keys = radix_sort_block(ka, kb, a.m, cnt, base, diff);
+    unsigned long long u2 = 0;
+    for (int j = a.m + tid; j < a.N; j += kSweepThreads) {
+      double acc = 0.0;
+      for (int c = 0; c < pop; ++c) acc = acc + a.cols[static_cast<size_t>(s_cols[c]) * a.N + j];
+      const double mean = acc / dpop;
+      if (a.ens_out && s == 0) a.ens_out[j] = mean;
+      const unsigned long long k = order_key(mean);
+      const int lo = lower_bound_u64(keys, a.m, k);
+      // upper bound: walk the (usually empty) run of equal keys; a long run (tie-heavy
+      // cohorts) falls back to the binary search
+      int hi = lo;
+      while (hi < a.m && hi - lo < 8 && keys[hi] == k) ++hi;
+      if (hi - lo == 8) hi = upper_bound_u64(keys, a.m, k);
+      u2 += a.sorted_is_pos ? (2ull * a.m - static_cast<unsigned long long>(lo + hi))
+                            : static_cast<unsigned long long>(lo + hi);
+    }
+    for (int off = 16; off > 0; off >>= 1) u2 += __shfl_xor_sync(0xffffffffu, u2, off);
+    if ((tid & 31) == 0) s_red[tid >> 5] = u2;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < kSweepThreads / 32; ++w) t += s_red[w];
+      const double u = static_cast<double>(t) * 0.5;
+      a.auc[s] = u / static_cast<double>(a.n_pos * a.n_neg);
+    }
+  }
+}
+
+size_t radix_smem(int m) { return sizeof(unsigned long long) * 2 * m + sizeof(unsigned) * (32 * 256 + 256); }
+bool radix_on(int m) {
+  static const bool env_on = !(getenv("HB_SWEEP_RADIX") && atoi(getenv("HB_SWEEP_RADIX")) == 0);
+  return env_on && m <= kRadixMax;
+}
+
 }  // namespace hb
 
 // ------------------------------------------------------------------ C-ABI
@@ -314,7 +482,9 @@ int run(hb_cohort* c, const uint8_t* d_bits, unsigned long long first, long long
   a.auc = c->d_auc;
   a.ens_out = host_ens ? c->d_ens : nullptr;
   const size_t smem = (c->p2 <= kSmemKeys) ? sizeof(unsigned long long) * c->p2 : 0;
-  if (c->p2 <= kSmemKeys)
+  if (radix_on(c->m))
+    sweep_auc_radix_kernel<<<grid, kSweepThreads, radix_smem(c->m), c->st>>>(a);
+  else if (c->p2 <= kSmemKeys)
     sweep_auc_kernel<true><<<grid, kSweepThreads, smem, c->st>>>(a);
   else
     sweep_auc_kernel<false><<<grid, kSweepThreads, smem, c->st>>>(a);
@@ -383,6 +553,10 @@ int hb_cohort_create(int device, const double* scores, const int8_t* labels, int
       cudaFuncSetAttribute(sweep_auc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(sizeof(unsigned long long) * kSmemKeys)) != cudaSuccess)
     rc = cfail(nullptr, HB_E_CUDA, "sweep kernel attribute setup failed");
+  if (rc == HB_OK && radix_on(c->m) &&
+      cudaFuncSetAttribute(sweep_auc_radix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(radix_smem(kRadixMax))) != cudaSuccess)
+    rc = cfail(nullptr, HB_E_CUDA, "sweep radix kernel attribute setup failed");
   if (rc != HB_OK) {
     hb_cohort_destroy(c);
     return rc;
