@@ -582,8 +582,8 @@ int hb_create(int device, const hb_config* cfg, hb_ctx** out) {
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   const size_t S = static_cast<size_t>(c->P) * c->leads;
   bool ok = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaMalloc(&c->ring, S * c->R * sizeof(float)) == cudaSuccess &&
-            cudaMemset(c->ring, 0, S * c->R * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&c->ring, S * (c->R + c->W) * sizeof(float)) == cudaSuccess &&  // + mirror of W
+            cudaMemset(c->ring, 0, S * (c->R + c->W) * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&c->staged_io[0], S * c->hop * sizeof(float)) == cudaSuccess &&
             cudaMalloc(&c->staged_io[1], S * c->hop * sizeof(float)) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess &&

@@ -198,7 +198,8 @@ cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int
 // *wpos, then (if xn != null) gather of the window ending at *wpos + n_new and
 // z-normalisation -> xn[lead][P][window] fp16.  raw_out (optional) receives the
 // raw gathered window [P][leads][window] fp32, stats (optional) mean/std.
-cudaError_t launch_ingest_window(const float* staged /*[P][leads][n_new]*/, float* ring /*[P][leads][R]*/,
+cudaError_t launch_ingest_window(const float* staged /*[P][leads][n_new]*/,
+                                 float* ring /*[P][leads][R + window]: ring + mirror of its first window slots*/,
                                  const long long* wpos, int P, int leads, int n_new, int R, int window,
                                  __half* xn /*[leads][xn_rows][roundup(window, 8)]*/, int xn_rows, float* raw_out,
                                  float* stats, cudaStream_t st);

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   pdl_wait();  // the ring cursor / rings / staging buffer belong to the previous tick's chain
   pdl_trigger();
   const long long wpos = *wpos_p;
-  float* rs = ring + static_cast<size_t>(s) * R;
+  float* rs = ring + static_cast<size_t>(s) * (R + W);
   const float* src = staged + static_cast<size_t>(s) * n_new;
   const int w0 = static_cast<int>(wpos % R);
   for (int i = threadIdx.x; i < n_new; i += blockDim.x) {
@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
     int j = w0 + i;
     if (j >= R) j -= R;
     rs[j] = v;
+    if (j < W) rs[R + j] = v;  // mirror: any window is then a contiguous run of [0, R + W)
     if (xn != nullptr && i >= n_new - W) win[W - n_new + i] = v;  // newest samples straight from staging
   }
   if (xn == nullptr) return;
@@ -101,11 +102,13 @@ __global__ void __launch_bounds__(kWinThreads) ingest_window_kernel(const float*
   }
 }
 
-// Register-resident variant for many streams (ingest_window_reg): T threads
-// per stream, thread t holds window samples t, t+T, ... (PER of them); the
-// loads are branch-free (predicated) so all PER are in flight at once, and
-// with T=256 eight streams share an SM.  Same arithmetic order as the shared-
-// memory kernel above except the two block sums (fixed order, T/32 partials).
+// Register-resident variant (ingest_window_reg): T threads per stream, thread
+// t holds window samples t, t+T, ... (PER of them).  The ring carries a mirror
+// of its first W slots after slot R-1, so after this tick's append the window
+// is one contiguous run: PER loads at a constant stride from one base register
+// (80 registers -> three 256-thread streams per SM).  Same arithmetic as the
+// shared-memory kernel above except the two block sums (fixed order, T/32
+// partials).
 template <int T>
 __device__ __forceinline__ float block_sum_t(float v, float* red) {
 #pragma unroll
@@ -121,7 +124,7 @@ __device__ __forceinline__ float block_sum_t(float v, float* red) {
 }
 
 template <int T, int PER>
-__global__ void __launch_bounds__(T) ingest_window_reg_kernel(const float* __restrict__ staged,
+__global__ void __launch_bounds__(T, 3) ingest_window_reg_kernel(const float* __restrict__ staged,
                                                               float* __restrict__ ring,
                                                               const long long* __restrict__ wpos_p, int leads,
                                                               int n_new, int R, int W, __half* __restrict__ xn,
@@ -134,32 +137,33 @@ __global__ void __launch_bounds__(T) ingest_window_reg_kernel(const float* __res
   pdl_wait();
   pdl_trigger();
   const long long wpos = *wpos_p;
-  float* rs = ring + static_cast<size_t>(s) * R;
+  float* rs = ring + static_cast<size_t>(s) * (R + W);
   const float* src = staged + static_cast<size_t>(s) * n_new;
   const long long start = wpos + n_new - W;
-  const int old_n = W - n_new;  // (this variant requires n_new <= W)
   const int r0 = static_cast<int>(((start % R) + R) % R);
+  // append this tick's samples (and their mirror), then read the whole window
+  // as one contiguous run of the mirrored ring: PER loads at a constant stride
+  // from one base (few live registers -> more streams per SM)
+  const int w0 = static_cast<int>(wpos % R);
+  for (int i = threadIdx.x; i < n_new; i += T) {
+    int j = w0 + i;
+    if (j >= R) j -= R;
+    const float v = src[i];
+    rs[j] = v;
+    if (j < W) rs[R + j] = v;
+  }
+  __syncthreads();
+  const float* win = rs + r0 + threadIdx.x;
   float v[PER];
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int i = threadIdx.x + k * T;
-    int j = r0 + i;
-    j -= (j >= R) ? R : 0;
-    const bool from_ring = i < old_n;
-    const float* ptr = from_ring ? rs + j : src + (i - old_n);
-    const bool ok = i < W && (!from_ring || start + i >= 0);
-    v[k] = ok ? __ldg(ptr) : 0.f;
+    v[k] = (i < W && start + i >= 0) ? win[k * T] : 0.f;
   }
   float part = 0.f;
 #pragma unroll
   for (int k = 0; k < PER; ++k) part += v[k];
-  const float mean = block_sum_t<T>(part, red) / static_cast<float>(W);  // (its barrier also orders the
-  const int w0 = static_cast<int>(wpos % R);                               //  ring reads before the append)
-  for (int i = threadIdx.x; i < n_new; i += T) {
-    int j = w0 + i;
-    if (j >= R) j -= R;
-    rs[j] = src[i];
-  }
+  const float mean = block_sum_t<T>(part, red) / static_cast<float>(W);
   float sq = 0.f;
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
