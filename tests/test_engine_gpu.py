@@ -174,3 +174,25 @@ def test_pipelined_submit_collect_matches_blocking_ticks():
             slot = nxt
     for (a, b, c), (x, y, z) in zip(ref, got):
         assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z)
+
+
+def test_many_ticks_across_ring_wraps():
+    """70 sliding ticks: the ring (R = roundup(W + hop, 256)) wraps twice; every tick's gathered
+    window stays bit-exact (the mirrored ring tail keeps each window one contiguous run) and the
+    last tick's scores match the oracle."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [0])
+    P, W, hop, n = 2, 7500, 250, 70
+    streams = _streams(P, W + n * hop, seed=7)
+    with EnsembleEngine(zoo, sel, P, hop=hop, keep_windows=True) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        for k in range(n):
+            end = W + k * hop
+            res = eng.tick(streams[:, :, end - hop:end])
+            if k % 7 == 0 or k == n - 1:
+                raw, _ = eng.last_windows()
+                for p in range(P):
+                    for lead in range(3):
+                        assert np.array_equal(raw[p, lead], windows.sliding_window(streams[p, lead], end, W)), k
+        _compare(res, *_oracle_tick(zoo, sel, streams, end))
