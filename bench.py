@@ -52,7 +52,7 @@ SLO_MS = 200.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=1000)  # >= 1000 ticks per config
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--patients", type=int, default=64, help="beds per GPU")
@@ -423,8 +423,8 @@ def run_b200(args):
     extras = {}
     if rank == 0 and world == 1 and not args.profile_only and not args.no_extras:
         eng.close()
-        extras["beds_1024"] = tick_at(zoo, sel, 1024, hop, local)
-        extras["c3_full_zoo_100_beds"] = tick_at(zoo, Selector.ones(60), 100, hop, local, K=10, warm=2)
+        extras["beds_1024"] = tick_at(zoo, sel, 1024, hop, local, K=200)
+        extras["c3_full_zoo_100_beds"] = tick_at(zoo, Selector.ones(60), 100, hop, local, K=50, warm=3)
         extras["profiler_sweep"] = sweep_bench(local)
 
     cfg = workload(args)
