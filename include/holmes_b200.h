@@ -209,6 +209,8 @@ int hb_op_stem(const void* xn, int P, int L, const float* w_host, const float* b
                void* stream);
 int hb_op_stem_q(const void* xn, int P, int L, const float* w_host, const float* b_host, int cout, void* out,
                  int out_q, void* stream);
+/* Micro-benchmark of the stem (K3) on zero data, G members x Pm rows: mean ms per launch. */
+int hb_bench_stem(int G, int Pm, int L, int cout, int out_q, int iters, float* ms_out);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,7 @@ _SIGS = {
     "hb_conv_head_mt": (C.c_int, [C.c_int] * 7),
     "hb_bench_conv_k": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _F]),
     "hb_op_stem_q": (C.c_int, [_P, C.c_int, C.c_int, _F, _F, C.c_int, _P, C.c_int, _P]),
+    "hb_bench_stem": (C.c_int, [C.c_int] * 6 + [_F]),
 }
 
 _lock = threading.Lock()

@@ -74,43 +74,6 @@ __device__ __forceinline__ PPTile pp_tile(const PPArgs& a, int tile) {
   return t;
 }
 
-// 8x8 transpose of fp16 values inside aligned 8-lane groups: lane r8 holds
-// row r8 (its channel) as 4 half2 registers
-// (columns 2k, 2k+1); afterwards it holds column r8 (channels 2k, 2k+1 in
-// register k).  Two register exchanges per 4x4 / 2x2 stage; the single-
-// element stage moves two halves per shuffle (byte permutes): 6 shuffles per
-// 8x8 block (an fp32 transpose takes 12 shuffles + 24 selects).
-__device__ __forceinline__ void transpose8_h2(uint32_t (&h)[4], int r8) {
-  {
-    const bool hi = (r8 & 4) != 0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const uint32_t recv = __shfl_xor_sync(0xffffffffu, hi ? h[k] : h[k + 2], 4);
-      if (hi) h[k] = recv; else h[k + 2] = recv;
-    }
-  }
-  {
-    const bool hi = (r8 & 2) != 0;
-#pragma unroll
-    for (int k = 0; k < 4; k += 2) {
-      const uint32_t recv = __shfl_xor_sync(0xffffffffu, hi ? h[k] : h[k + 1], 2);
-      if (hi) h[k] = recv; else h[k + 1] = recv;
-    }
-  }
-  {
-    const bool hi = (r8 & 1) != 0;
-    const uint32_t s_send = hi ? 0x5410u : 0x7632u;
-    const uint32_t s_a = hi ? 0x3254u : 0x5410u;
-    const uint32_t s_b = hi ? 0x3276u : 0x7610u;
-#pragma unroll
-    for (int k = 0; k < 4; k += 2) {
-      const uint32_t r = __shfl_xor_sync(0xffffffffu, __byte_perm(h[k], h[k + 1], s_send), 1);
-      h[k] = __byte_perm(h[k], r, s_a);
-      h[k + 1] = __byte_perm(h[k + 1], r, s_b);
-    }
-  }
-}
-
 // Shortcut row load (HB_PP_DBG & 64: L2-only ld.global.cg instead of the
 // read-only L1 path).
 __device__ __forceinline__ uint4 ldres_sel(const uint4* p, bool cg) { return cg ? __ldcg(p) : __ldg(p); }

@@ -1168,6 +1168,52 @@ int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode,
   return rc;
 }
 
+// Back-to-back stem launches (zero data) for timing experiments: G members of Pm rows.
+int hb_bench_stem(int G, int Pm, int L, int cout, int out_q, int iters, float* ms_out) {
+  if (init_kernels() != cudaSuccess) return fail(nullptr, HB_E_CUDA, "kernel attribute setup failed");
+  if (G < 1 || G > kMaxGroup || Pm < 1 || L < 16 || iters < 1) return fail(nullptr, HB_E_INVALID, "bad stem bench shape");
+  hb_ctx* none = nullptr;
+  const int Lp = round_up(L, 8);
+  void *x = nullptr, *w = nullptr, *b = nullptr, *out = nullptr;
+  const size_t out_b = static_cast<size_t>(G) * Pm * cout * plane_rows_max(L) * 2;
+  CK(none, cudaMalloc(&x, static_cast<size_t>(G) * Pm * Lp * 2));
+  CK(none, cudaMemset(x, 0, static_cast<size_t>(G) * Pm * Lp * 2));
+  CK(none, cudaMalloc(&w, sizeof(float) * cout * kTaps));
+  CK(none, cudaMemset(w, 0, sizeof(float) * cout * kTaps));
+  CK(none, cudaMalloc(&b, sizeof(float) * cout));
+  CK(none, cudaMemset(b, 0, sizeof(float) * cout));
+  CK(none, cudaMalloc(&out, out_b));
+  std::vector<StemMember> m(G);
+  for (int g = 0; g < G; ++g)
+    m[g] = StemMember{static_cast<const __half*>(x) + static_cast<size_t>(g) * Pm * Lp, static_cast<float*>(w),
+                      static_cast<float*>(b)};
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaError_t ce = cudaSuccess;
+  for (int i = 0; i < 3 && ce == cudaSuccess; ++i)
+    ce = launch_stem(m.data(), G, Lp, Pm, L, out_q, cout, (kTaps - 1) / 2, static_cast<__half*>(out), st);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < iters && ce == cudaSuccess; ++i)
+    ce = launch_stem(m.data(), G, Lp, Pm, L, out_q, cout, (kTaps - 1) / 2, static_cast<__half*>(out), st);
+  cudaEventRecord(e1, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_out = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  cudaFree(x);
+  cudaFree(w);
+  cudaFree(b);
+  cudaFree(out);
+  if (ce != cudaSuccess) return fail(none, HB_E_CUDA, cudaGetErrorString(ce));
+  return HB_OK;
+}
+
 int hb_bench_conv(int P, int cin, int cout, int lin, int stride, int res_mode, int iters, float* ms_out) {
   return hb_bench_conv_k(P, cin, cout, lin, stride, res_mode, KIND_TC, iters, ms_out);
 }

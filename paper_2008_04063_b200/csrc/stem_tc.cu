@@ -26,6 +26,9 @@
 // Accumulators rotate over kAcc TMEM buffers.  Every member of the group keeps
 // its B image (fp16 weights) and bias resident in smem, so member changes cost
 // nothing.
+#include <cstdlib>
+#include <cstring>
+
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
@@ -222,16 +225,18 @@ static size_t stem_smem_bytes(int G, int n_mma, int cout) {
          static_cast<size_t>((G * cout + 1) & ~1) * 4 + (3 * kStages + 2 * kAcc) * 8 + 16;
 }
 
+cudaError_t init_stem_pp_kernel();
 cudaError_t init_stem_kernel() {
-  return cudaFuncSetAttribute(stem_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  const cudaError_t e = cudaFuncSetAttribute(stem_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  return e != cudaSuccess ? e : init_stem_pp_kernel();
 }
 
 using EncodeTiledFnStem = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
-                        __half* out, cudaStream_t st) {
+static cudaError_t launch_stem_toeplitz(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q,
+                                       int cout, int pad, __half* out, cudaStream_t st) {
   if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup || pad > 8 || (x_stride * 2) % 16) return cudaErrorInvalidValue;
   StemTcArgs a;
   // one 2-D view {L samples, rows} over every member's windows (they share the buffer and its row stride)
@@ -282,6 +287,369 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.num_tiles < sms ? a.num_tiles : sms;
   return launch_pdl(stem_tc_kernel, dim3(grid), dim3(kStemThreads), stem_smem_bytes(G, a.n_mma, cout), st, tm, a);
+}
+
+
+// ---------------------------------------------------------------------------
+// K3, phase-shifted-weights form (the default; HB_STEM=0 selects the builder
+// kernel above).  Output position l = l0 + 8n + j, n in [0, 128) on the TMEM
+// lanes, phase j in [0, 8) and channel c on the columns:
+//   D[n, (j, c)] = sum_k' A[n, k'] B_j[c, k'],  k' in [0, 32)
+//   A[n, k'] = x[l0 - 8 + 8n + k'],   B_j[c, k'] = W[c, k' - j - 8 + pad]
+// A is the window segment itself: in the canonical K-major no-swizzle layout
+// row n of a core matrix sits at 16 B * n (8 samples) and the next K core
+// matrix at +16 B, so LBO = 16 B and SBO = 128 B turn the plain sample array
+// (one 16-B aligned TMA segment per tile) into the Toeplitz operand; the
+// sub-16-B shifts of the 8 phases live in 8 shifted weight images instead
+// (TMA coordinates and descriptor addresses are 16-B granular).  Two K=16
+// MMAs per phase.  With positions on the lanes the epilogue needs no
+// transpose: a thread holds 8 channels of positions l and l + Q (phases j and
+// j + Q), the two halves of one 32-B sector of the consumer's Q-phase layout:
+// one 256-bit store (Q >= 8: two 128-bit stores into separate sub-planes).
+// Warp roles as in K4b: 0 TMA, 1 MMA, 2 TMEM, 4-19 four epilogue warpgroups
+// (buffer = ew & 1, half of the tile's (phase pair, 8-channel) units = ew >> 1).
+constexpr int kStemPPThreads = 640;
+constexpr int kStemPPStages = 8;
+constexpr int kStemSeg = 2560;  // one tile's window segment: 5 boxes of 256 samples (1048 used)
+
+struct StemPPArgs {
+  StemMember m[kMaxGroup];
+  int x_row0[kMaxGroup];
+  int G, Pm, L, C, Ceff, pad, out_qs, out_lq, out_rows;
+  int J, dd, paired, groups_per_blk, nt_per_row, num_tiles, stage_bytes, n_stages;
+  int dbg;  // HB_STEM_DBG (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA
+  __half* out;
+};
+
+// (lo, hi) -> max(0, .) rounded to fp16, lo in the low half (one F2FP.RELU)
+__device__ __forceinline__ uint32_t pack_relu_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void st_global_256(void* p, const uint32_t (&v)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kStemPPThreads, 1)
+    stem_pp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ StemPPArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int wimg = a.Ceff * 32;                                   // one (phase, k-step) B image
+  uint8_t* sW = smem;                                             // [G][8 phases][2 k-steps][k-half][Ceff][16 B]
+  uint8_t* sX = sW + static_cast<size_t>(a.G) * 16 * wimg;        // [n_stages][kStemSeg]
+  float* sBias = reinterpret_cast<float*>(sX + a.n_stages * kStemSeg);  // [G][Ceff]
+  uint64_t* st_full = reinterpret_cast<uint64_t*>(sBias + a.G * a.Ceff);
+  uint64_t* st_empty = st_full + a.n_stages;
+  uint64_t* acc_full = st_empty + a.n_stages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* sUnit = reinterpret_cast<int*>(tmem_holder + 4);           // [64] epilogue unit -> (phase ja, c8)
+  float* sRaw = reinterpret_cast<float*>(sUnit + 64);             // [G][16][C] staged taps
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < a.n_stages; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 256);  // two epilogue warpgroups per buffer
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, 512);
+  // B images and biases: constants, built before the dependency wait (taps
+  // staged through shared memory so the global reads are coalesced)
+  for (int i = tid; i < a.G * a.C * kTaps; i += kStemPPThreads) {  // -> [g][tap][channel]: conflict-free reads below
+    const int g = i / (a.C * kTaps), rem = i - g * a.C * kTaps;
+    const int n = rem >> 4, t = rem & 15;
+    sRaw[(g * kTaps + t) * a.C + n] = a.m[g].w[rem];
+  }
+  for (int i = tid; i < a.G * a.Ceff; i += kStemPPThreads) {
+    const int g = i / a.Ceff, c = i - g * a.Ceff;
+    sBias[i] = c < a.C ? a.m[g].b[c] : 0.f;
+  }
+  if (tid < (a.J / 2) * (a.C / 8)) {  // unit u = (phase pair pi, 8-channel group c8), pair = (ja, ja + dd)
+    const int pi = tid / (a.C / 8), c8 = tid - pi * (a.C / 8);
+    sUnit[tid] = ((pi / a.dd) * 2 * a.dd + (pi % a.dd)) | (c8 << 8);
+  }
+  __syncthreads();
+  const int rows_per_g = 8 * 2 * 2 * a.Ceff;  // 16-B rows: (phase, k-step, k-half, n)
+  for (int i = tid; i < a.G * rows_per_g; i += kStemPPThreads) {
+    const int g = i / rows_per_g;
+    int r = i - g * rows_per_g;
+    const int n = r % a.Ceff;
+    r /= a.Ceff;
+    const int h = r & 1, s = (r >> 1) & 1, j = r >> 2;
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = 16 * s + 8 * h + e - j - 8 + a.pad;
+      v[e] = __float2half_rn(n < a.C && t >= 0 && t < kTaps ? sRaw[(g * kTaps + t) * a.C + n] : 0.f);
+    }
+    *reinterpret_cast<uint4*>(sW + static_cast<size_t>(i) * 16) = *reinterpret_cast<const uint4*>(v);
+  }
+  fence_proxy_async();  // B images are read by the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+  const int cols_buf = a.J * a.Ceff;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      pdl_wait();  // x is the window kernel's output
+      int st = 0;
+      uint32_t sph = 0;
+      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+        const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
+        const int nb = rt / a.groups_per_blk;
+        const int g = row / a.Pm, p = row - g * a.Pm;
+        mbar_wait(&st_empty[st], sph ^ 1u, 331);
+        if (a.dbg & 4) {
+          mbar_arrive(&st_full[st]);
+        } else {
+          mbar_arrive_expect_tx(&st_full[st], static_cast<uint32_t>(kStemSeg));
+          uint8_t* dst = sX + st * kStemSeg;
+          for (int b = 0; b < kStemSeg / 512; ++b)  // samples [l0 - 8, l0 + 1272), 16-B aligned start
+            tma_load_2d(dst + 512 * b, &tmX, &st_full[st], nb * 1024 - 8 + 256 * b, a.x_row0[g] + p);
+        }
+        if (++st == a.n_stages) {
+          st = 0;
+          sph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA
+    const uint32_t idesc = make_idesc_f16(kBM, a.Ceff);
+    int st = 0, acc = 0;
+    uint32_t sph = 0, accph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
+      const int g = row / a.Pm, jg = rt % a.groups_per_blk;
+      mbar_wait(&st_full[st], sph, 332);
+      mbar_wait(&acc_empty[acc], accph ^ 1u, 333);
+      tc_fence_after();
+      const uint32_t xs = smem_u32(sX + st * kStemSeg);
+      const uint32_t ws = smem_u32(sW + static_cast<size_t>(g) * 16 * wimg);
+      const uint32_t d0 = tmem_base + static_cast<uint32_t>(acc * cols_buf);
+      for (int jj = 0; jj < a.J; ++jj) {
+        const int j = jg * a.J + jj;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const uint64_t ad = make_desc(xs + static_cast<uint32_t>(32 * s), 16, 128);
+          const uint64_t bd = make_desc(ws + static_cast<uint32_t>((j * 2 + s) * wimg), a.Ceff * 16, 128);
+          if (!(a.dbg & 2) && elect_one())
+            mma_f16_ss(d0 + static_cast<uint32_t>(jj * a.Ceff), ad, bd, idesc, static_cast<uint32_t>(s));
+          __syncwarp();
+        }
+      }
+      if (elect_one()) {
+        mma_commit(&st_empty[st]);
+        mma_commit(&acc_full[acc]);
+      }
+      __syncwarp();
+      if (++st == a.n_stages) {
+        st = 0;
+        sph ^= 1u;
+      }
+      if (++acc == 2) {
+        acc = 0;
+        accph ^= 1u;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- epilogue
+    const int ew = (static_cast<int>(warp) - 4) >> 2;
+    const int eb = ew & 1;
+    const int wq = static_cast<int>(warp) & 3;
+    const int n = wq * 32 + static_cast<int>(lane);  // TMEM lane = position block
+    const int nc8 = a.C / 8;
+    const int units = (a.J / 2) * nc8;  // (phase pair, 8-channel group)
+    const int u_lo = (ew >> 1) ? (units + 1) / 2 : 0, u_hi = (ew >> 1) ? units : (units + 1) / 2;
+    uint32_t accph = 0;
+    pdl_wait();  // the output buffer may still be read by the previous tick's layers
+    for (int tile = blockIdx.x + eb * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+      const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
+      const int nb = rt / a.groups_per_blk, jg = rt - nb * a.groups_per_blk;
+      const int g = row / a.Pm;
+      const int lbase = nb * 1024 + 8 * n + jg * a.J;
+      mbar_wait(&acc_full[eb], accph, 334);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * cols_buf);
+      // Units run through two register sets: the next unit's TMEM loads are in
+      // flight while the current one is converted and stored (tcgen05.wait::ld
+      // waits for every outstanding load, so the sets alternate).
+      auto unit_cols = [&](int u, uint32_t& ca, uint32_t& cb) {
+        const int code = sUnit[u];
+        ca = tb + static_cast<uint32_t>((code & 255) * a.Ceff + (code >> 8) * 8);
+        cb = ca + static_cast<uint32_t>(a.dd * a.Ceff);
+      };
+      auto issue = [&](int u, uint32_t (&ra)[8], uint32_t (&rb)[8]) {
+        uint32_t ca, cb;
+        unit_cols(u, ca, cb);
+        tmem_ld8_nw(ca, ra);
+        tmem_ld8_nw(cb, rb);
+      };
+      auto store = [&](int u, const uint32_t (&ra)[8], const uint32_t (&rb)[8]) {
+        const int code = sUnit[u];
+        const int ja = code & 255, c8 = code >> 8, jb = ja + a.dd;
+        const float4 b0 = *reinterpret_cast<const float4*>(sBias + g * a.Ceff + c8 * 8);
+        const float4 b1 = *reinterpret_cast<const float4*>(sBias + g * a.Ceff + c8 * 8 + 4);
+        const float bias[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const int la = lbase + ja, lb = lbase + jb;
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[k] = pack_relu_f16x2(__uint_as_float(ra[2 * k]) + bias[2 * k], __uint_as_float(ra[2 * k + 1]) + bias[2 * k + 1]);
+          v[4 + k] = pack_relu_f16x2(__uint_as_float(rb[2 * k]) + bias[2 * k], __uint_as_float(rb[2 * k + 1]) + bias[2 * k + 1]);
+        }
+        if (la >= a.L) v[0] = v[1] = v[2] = v[3] = 0u;  // the layout's zero padding [L, out_rows)
+        if (lb >= a.L) v[4] = v[5] = v[6] = v[7] = 0u;
+        if (a.dbg & 1) return;
+        const size_t plane = static_cast<size_t>(row) * nc8 + c8;
+        __half* pa = a.out + q_off(plane, a.out_qs, a.out_lq, la);
+        if (a.paired && lb < a.out_rows) {
+          st_global_256(pa, v);  // l and l + Q: adjacent rows of one sub-plane
+        } else {
+          if (la < a.out_rows) *reinterpret_cast<uint4*>(pa) = make_uint4(v[0], v[1], v[2], v[3]);
+          if (lb < a.out_rows)
+            *reinterpret_cast<uint4*>(a.out + q_off(plane, a.out_qs, a.out_lq, lb)) = make_uint4(v[4], v[5], v[6], v[7]);
+        }
+      };
+      auto release = [&]() {
+        tc_fence_before();
+        mbar_arrive(&acc_empty[eb]);
+      };
+      uint32_t xa[8], xb[8], ya[8], yb[8];
+      if (u_lo < u_hi) issue(u_lo, xa, xb);
+      for (int u = u_lo; u < u_hi; u += 2) {
+        tmem_wait_ld();  // set x (unit u) landed
+        if (u + 1 < u_hi) {
+          issue(u + 1, ya, yb);
+        } else {
+          release();
+        }
+        store(u, xa, xb);
+        if (u + 1 >= u_hi) break;
+        tmem_wait_ld();  // set y (unit u + 1) landed
+        if (u + 2 < u_hi) {
+          issue(u + 2, xa, xb);
+        } else {
+          release();
+        }
+        store(u + 1, ya, yb);
+      }
+      if (u_lo >= u_hi) {  // no units for this warpgroup: release the buffer all the same
+        tc_fence_before();
+        mbar_arrive(&acc_empty[eb]);
+      }
+      accph ^= 1u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+cudaError_t init_stem_pp_kernel() {
+  return cudaFuncSetAttribute(stem_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+}
+
+cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
+                        __half* out, cudaStream_t st) {
+  static const int which = getenv("HB_STEM") ? atoi(getenv("HB_STEM")) : 1;
+  if (!which) return launch_stem_toeplitz(members, G, x_stride, Pm, L, out_q, cout, pad, out, st);
+  if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup || pad < 0 || pad > 8 || (x_stride * 2) % 16 ||
+      out_q < 1 || out_q > 32 || (out_q & (out_q - 1)))
+    return cudaErrorInvalidValue;
+  StemPPArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.G = G;
+  a.Pm = Pm;
+  a.L = L;
+  a.C = cout;
+  a.Ceff = cout < 16 ? 16 : round_up(cout, 16);
+  a.pad = pad;
+  a.out_qs = ilog2(out_q);
+  a.out_lq = lq_Q(L, out_q);
+  a.out_rows = act_rows_q(L, out_q);
+  a.J = 8;  // phases per tile (8, 4 or 2): J * Ceff TMEM columns per accumulator
+  while (a.J > 2 && a.J * a.Ceff > 256) a.J >>= 1;
+  // two phases per tile (C > 64) leave too little per accumulator: the builder kernel is faster there
+  if (a.J < 4) return launch_stem_toeplitz(members, G, x_stride, Pm, L, out_q, cout, pad, out, st);
+  a.dd = out_q < a.J ? out_q : 1;  // pair phases j, j + dd
+  a.paired = a.dd == out_q;        // ... which are adjacent 16-B rows of the layout
+  a.groups_per_blk = 8 / a.J;
+  a.nt_per_row = ((a.out_rows + 1023) / 1024) * a.groups_per_blk;
+  a.stage_bytes = kStemSeg;
+  a.n_stages = kStemPPStages;
+  a.dbg = getenv("HB_STEM_DBG") ? atoi(getenv("HB_STEM_DBG")) : 0;
+  // members per launch: every member's 16 B images stay resident
+  const size_t per_g = static_cast<size_t>(16) * a.Ceff * 32 + a.Ceff * 4 + static_cast<size_t>(cout) * kTaps * 4;
+  const size_t fixed = static_cast<size_t>(a.n_stages) * kStemSeg + (2 * a.n_stages + 4) * 8 + 16 + 64 * 4;
+  if ((a.J / 2) * (cout / 8) > 64) return cudaErrorInvalidValue;
+  const int gmax = static_cast<int>((kSmemLimit - fixed) / per_g);
+  if (gmax < 1) return cudaErrorInvalidValue;
+  static EncodeTiledFnStem enc = nullptr;
+  if (!enc) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return cudaErrorNotSupported;
+    enc = reinterpret_cast<EncodeTiledFnStem>(fp);
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t plane_elems = static_cast<size_t>(a.out_rows) * 8;
+  for (int g0 = 0; g0 < G; g0 += gmax) {
+    const int Gs = G - g0 < gmax ? G - g0 : gmax;
+    const __half* base = members[g0].x;
+    for (int g = 1; g < Gs; ++g) base = members[g0 + g].x < base ? members[g0 + g].x : base;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return cudaErrorInvalidValue;
+    long long rows = 0;
+    for (int g = 0; g < Gs; ++g) {
+      a.m[g] = members[g0 + g];
+      const long long off = members[g0 + g].x - base;
+      if (off % x_stride) return cudaErrorInvalidValue;
+      a.x_row0[g] = static_cast<int>(off / x_stride);
+      rows = a.x_row0[g] + Pm > rows ? a.x_row0[g] + Pm : rows;
+    }
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(x_stride) * 2};
+    const cuuint32_t box[2] = {256, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    a.G = Gs;
+    a.num_tiles = Gs * Pm * a.nt_per_row;
+    a.out = out + static_cast<size_t>(g0) * Pm * (cout / 8) * plane_elems;
+    const int grid = a.num_tiles < sms ? a.num_tiles : sms;
+    const cudaError_t e =
+        launch_pdl(stem_pp_kernel, dim3(grid), dim3(kStemPPThreads), fixed + Gs * per_g, st, tm, a);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace hb

@@ -124,11 +124,12 @@ def test_tc_conv_q_layouts(out_q, res_q):
     assert q_padding_zero(out, lout, out_q)
 
 
-@pytest.mark.parametrize("cout,out_q", [(32, 4), (64, 2), (16, 8)])
-def test_stem_q_layout(cout, out_q):
+@pytest.mark.parametrize("cout,out_q,n", [(32, 4, 7500), (64, 2, 7500), (16, 8, 7500), (8, 1, 7500), (128, 1, 7500),
+                                          (32, 1, 1001), (32, 2, 999), (64, 4, 1250), (16, 16, 777), (24, 4, 600), (48, 2, 1500), (128, 2, 500)])
+def test_stem_q_layout(cout, out_q, n):
     L = _lib()
-    g = torch.Generator().manual_seed(cout + out_q)
-    P, n = 2, 7500
+    g = torch.Generator().manual_seed(cout + out_q + n)
+    P = 2
     x = _rand((P, n), g)
     w = _rand((cout, 1, 16), g, 0.25)
     b = _rand((cout,), g, 0.1)
