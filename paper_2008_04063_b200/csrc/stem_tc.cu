@@ -26,6 +26,7 @@
 // Accumulators rotate over kAcc TMEM buffers.  Every member of the group keeps
 // its B image (fp16 weights) and bias resident in smem, so member changes cost
 // nothing.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -573,7 +574,7 @@ cudaError_t init_stem_pp_kernel() {
 
 cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
                         __half* out, cudaStream_t st) {
-  static const int which = getenv("HB_STEM") ? atoi(getenv("HB_STEM")) : 1;
+  const int which = getenv("HB_STEM") ? atoi(getenv("HB_STEM")) : 1;  // read per launch (tests switch it)
   if (!which) return launch_stem_toeplitz(members, G, x_stride, Pm, L, out_q, cout, pad, out, st);
   if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup || pad < 0 || pad > 8 || (x_stride * 2) % 16 ||
       out_q < 1 || out_q > 32 || (out_q & (out_q - 1)))
@@ -604,7 +605,8 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
   const size_t per_g = static_cast<size_t>(16) * a.Ceff * 32 + a.Ceff * 4 + static_cast<size_t>(cout) * kTaps * 4;
   const size_t fixed = static_cast<size_t>(a.n_stages) * kStemSeg + (2 * a.n_stages + 4) * 8 + 16 + 64 * 4;
   if ((a.J / 2) * (cout / 8) > 64) return cudaErrorInvalidValue;
-  const int gmax = static_cast<int>((kSmemLimit - fixed) / per_g);
+  int gmax = static_cast<int>((kSmemLimit - fixed) / per_g);
+  if (const char* cap = getenv("HB_STEM_GMAX")) gmax = std::min(gmax, std::max(1, atoi(cap)));  // test knob: split launches
   if (gmax < 1) return cudaErrorInvalidValue;
   static EncodeTiledFnStem enc = nullptr;
   if (!enc) {

@@ -145,6 +145,31 @@ def test_patient_chunking_is_bit_identical(monkeypatch):
     assert np.array_equal(outs[0].ens_prob, outs[1].ens_prob)
 
 
+@pytest.mark.parametrize("knob", [("HB_STEM_GMAX", "1"), ("HB_STEM", "0")])
+def test_stem_launch_variants_are_bit_identical(monkeypatch, knob):
+    """The stem split into one launch per member (HB_STEM_GMAX=1) gives bit-identical outputs; the
+    builder stem kernel (HB_STEM=0) agrees within fp32 summation order."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, C2)
+    P, W, hop = 5, 7500, 250
+    streams = _streams(P, W + hop, seed=21)
+    outs = []
+    for env in (None, knob):
+        if env:
+            monkeypatch.setenv(*env)
+        with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+            eng.ingest(streams[:, :, :W - hop])
+            eng.tick(streams[:, :, W - hop:W])
+            outs.append(eng.tick(streams[:, :, W:W + hop]))
+    if knob[0] == "HB_STEM_GMAX":
+        assert np.array_equal(outs[0].member_logits, outs[1].member_logits)
+        assert np.array_equal(outs[0].ens_prob, outs[1].ens_prob)
+    else:
+        assert np.allclose(outs[0].member_logits, outs[1].member_logits, rtol=0, atol=2e-2)
+        assert np.allclose(outs[0].ens_prob, outs[1].ens_prob, rtol=0, atol=1e-3)
+
+
 def test_pipelined_submit_collect_matches_blocking_ticks():
     """submit(t+1) before collect(t): same outputs, bit for bit, as one blocking tick per step;
     a third submit while both slots hold uncollected ticks is refused."""
