@@ -109,12 +109,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       mbar_init(&acc_empty[i], 256);  // two epilogue warpgroups per buffer
     }
     fence_barrier_init();
+    // the first weight image (immutable, so before the dependency wait) goes out
+    // right behind the barrier init: its latency hides the rest of the prologue
+    if (static_cast<int>(blockIdx.x) < a.num_tiles) {
+      const uint8_t* src = a.wimg + static_cast<size_t>(pp_tile(a, blockIdx.x).g) * a.w_stride;
+      mbar_arrive_expect_tx(w_full, a.w_bytes);
+      for (uint32_t off = 0; off < a.w_bytes; off += 32768u)
+        bulk_load(sW + off, src + off, (a.w_bytes - off) < 32768u ? (a.w_bytes - off) : 32768u, w_full);
+    }
   }
   if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
-  for (int i = threadIdx.x; i < a.G * a.cout; i += blockDim.x) {
-    const int g = i / a.cout;
-    s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -132,11 +136,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           bulk_load(sW + off, src + off, n, w_full);
         }
       };
-      int loaded_g = -1, reloads = 0;
-      if (static_cast<int>(blockIdx.x) < a.num_tiles) {  // weights are immutable: before the dependency wait
-        loaded_g = pp_tile(a, blockIdx.x).g;
-        load_w(loaded_g);
-      }
+      int loaded_g = static_cast<int>(blockIdx.x) < a.num_tiles ? pp_tile(a, blockIdx.x).g : -1, reloads = 0;
       pdl_wait();
       int st = 0;
       uint32_t sph = 0;
@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int res_groups = a.res_c / 8;
     const int nch = a.nb / 16;  // 16-column chunks of the tile; this warpgroup takes half
     const int c_lo = (ew >> 1) * (nch / 2), c_hi = c_lo + nch / 2;
+    for (int i = static_cast<int>(threadIdx.x) - 128; i < a.G * a.cout; i += kPPThreads - 128) {
+      const int g = i / a.cout;
+      s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
+    }
+    named_bar_sync(1, kPPThreads - 128);  // the epilogue warps alone: off the producer's path
     uint32_t accph = 0;
     const bool eprof = (a.dbg & 16) && a.prof && warp == 4 && lane == 0;
     unsigned long long e_wait = 0, e_work = 0, e_start = eprof ? clock64() : 0;
