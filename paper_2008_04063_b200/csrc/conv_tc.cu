@@ -208,16 +208,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_init(&acc_empty[i], 128);  // one epilogue warpgroup per buffer
     }
     fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
-  const bool smem_bias = a.sb_len > 0;  // every member's bias / fc cached in smem
-  if (smem_bias) {
-    for (int i = threadIdx.x; i < a.G * a.bn; i += blockDim.x) {
-      const int g = i / a.bn, c = i - g * a.bn;
-      s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + c];
-      s_fc[i] = a.fc_w ? a.fc_w[static_cast<size_t>(g) * a.cout + (c < a.cout ? c : 0)] : 0.f;
+    // Weights are immutable: the first tile's resident B goes out right behind
+    // the barrier init (before the dependency wait), hiding the prologue.
+    if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {
+      const TileIdx t0 = decode_tile(a, blockIdx.x);
+      for (int kc = 0; kc < a.n_kchunks; ++kc) {
+        mbar_arrive_expect_tx(&b_full[kc], a.b_chunk_bytes);
+        bulk_load(sB + static_cast<size_t>(kc) * a.b_chunk_bytes,
+                  a.wpack + static_cast<size_t>(t0.g) * a.wpack_stride +
+                      (static_cast<size_t>(t0.nt) * a.n_kchunks + kc) * a.b_chunk_bytes,
+                  a.b_chunk_bytes, &b_full[kc]);
+      }
     }
   }
+  if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
+  const bool smem_bias = a.sb_len > 0;  // every member's bias / fc cached in smem (filled by the epilogue warps)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -242,14 +247,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         return a.wpack + static_cast<size_t>(t.g) * a.wpack_stride +
                (static_cast<size_t>(t.nt) * a.n_kchunks + kc) * a.b_chunk_bytes;
       };
-      // Weights are immutable: the first tile's resident B goes out before the
-      // dependency wait, overlapping the previous layer's tail.
-      if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {
+      if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {  // loaded in the prologue
         const TileIdx t0 = decode_tile(a, blockIdx.x);
-        for (int kc = 0; kc < a.n_kchunks; ++kc) {
-          mbar_arrive_expect_tx(&b_full[kc], a.b_chunk_bytes);
-          bulk_load(sB + static_cast<size_t>(kc) * a.b_chunk_bytes, b_src(t0, kc), a.b_chunk_bytes, &b_full[kc]);
-        }
         loaded_key = t0.g * a.n_ntiles + t0.nt;
       }
       pdl_wait();
@@ -433,6 +432,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const bool eprof = (a.dbg & 8) && a.prof && wq == 0 && lane == 0 && eg == 0;
     unsigned long long e_wait = 0, e_work = 0, et0 = 0, e_start = eprof ? clock64() : 0;
     uint32_t xround = 0;  // exchange buffer parity, alternates every round across tiles
+    if (smem_bias) {
+      for (int i = static_cast<int>(threadIdx.x) - 128; i < a.G * a.bn; i += static_cast<int>(blockDim.x) - 128) {
+        const int g = i / a.bn, c = i - g * a.bn;
+        s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + c];
+        s_fc[i] = a.fc_w ? a.fc_w[static_cast<size_t>(g) * a.cout + (c < a.cout ? c : 0)] : 0.f;
+      }
+      named_bar_sync(3, blockDim.x - 128);  // the epilogue warps alone (ids 1, 2: per-warpgroup exchange)
+    }
     pdl_wait();
     for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
       const TileIdx ti = decode_tile(a, tile);
