@@ -1,5 +1,9 @@
 // K3: the stem conv (1 input channel -> w channels, 16 taps, "same" padding)
-// + folded BN bias + ReLU on tcgen05 tensor cores.
+// + folded BN bias + ReLU on tcgen05 tensor cores.  Two kernels:
+//   stem_pp_kernel (further down, the default for w <= 64): the window segment
+//     itself is the MMA operand, the phase shifts live in shifted weight images;
+//   stem_tc_kernel (this first part, w = 128 or HB_STEM=0): Toeplitz rows built
+//     in shared memory, described here.
 //
 // With one input channel the whole 16-tap receptive field is exactly one
 // kind::f16 K-step, so a tile of 128 output positions is ONE MMA:
@@ -317,7 +321,7 @@ struct StemPPArgs {
   StemMember m[kMaxGroup];
   int x_row0[kMaxGroup];
   int G, Pm, L, C, Ceff, pad, out_qs, out_lq, out_rows;
-  int J, dd, paired, groups_per_blk, nt_per_row, num_tiles, stage_bytes, n_stages;
+  int J, dd, paired, groups_per_blk, nt_per_row, num_tiles, n_stages;
   int dbg;  // HB_STEM_DBG (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA
   __half* out;
 };
@@ -598,7 +602,6 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
   a.paired = a.dd == out_q;        // ... which are adjacent 16-B rows of the layout
   a.groups_per_blk = 8 / a.J;
   a.nt_per_row = ((a.out_rows + 1023) / 1024) * a.groups_per_blk;
-  a.stage_bytes = kStemSeg;
   a.n_stages = kStemPPStages;
   a.dbg = getenv("HB_STEM_DBG") ? atoi(getenv("HB_STEM_DBG")) : 0;
   // members per launch: every member's 16 B images stay resident
