@@ -49,6 +49,8 @@
 // D[(p', c), n].  Other shortcuts (maxpool, wider phases) are read by the
 // epilogue.  A member's last conv writes no output: the epilogue folds
 // mean-pool . FC into one partial per (tile, column half, warp).
+#include <functional>
+
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
@@ -270,8 +272,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const bool has_res = a.res_mode != 0 && g8 * 8 < a.res_c;
     const int out_groups = a.cout / 8;
     const int res_groups = a.res_c / 8;
-    const int nch = a.nb / 16;  // 16-column chunks of the tile; this warpgroup takes half
-    const int c_lo = (ew >> 1) * (nch / 2), c_hi = c_lo + nch / 2;
+    const int nch = a.nb / 16;  // 16-column chunks of the tile; this warpgroup takes half (the first the larger)
+    const int c_lo = (ew >> 1) ? (nch + 1) / 2 : 0, c_hi = (ew >> 1) ? nch : (nch + 1) / 2;
     for (int i = static_cast<int>(threadIdx.x) - 128; i < a.G * a.cout; i += kPPThreads - 128) {
       const int g = i / a.cout;
       s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
@@ -484,19 +486,24 @@ static EncodeTiledFnPP get_encode_pp() {
 // Columns per tile: the largest N whose operands fit with >= 2 stages, then
 // the one that minimises (waves x per-tile cost) -- small layers at serving
 // batch sizes prefer narrower tiles over a ragged last wave.  HB_PP_NB forces.
-static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const int* fits) {
+// Column tile N (a multiple of 16, 64..256): per-tile time ~ N + 171 column
+// units (the fixed part measured as N=128 tiles costing 1.4x per column of
+// N=256 ones: A is re-read per MMA), times the waves of tiles over the SMs.
+// Widths between the powers of two trim the padding of awkward rows (L = 7500
+// gives 1875 / 938 / 469 columns: 240-wide tiles instead of 256 drop the
+// 9 % padded columns to 2 %).
+static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits) {
   static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
-  const int cands[3] = {256, 128, 64};
-  const double cost[3] = {1.0, 1.4, 2.0};  // per-column MMA cost (measured: A is re-read per MMA, N=128 runs ~1.4x slower per column)
+  static const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
   int best = 0;
   double best_t = 1e30;
-  for (int k = 0; k < 3; ++k) {
-    const int nb = cands[k];
-    if (!fits[k]) continue;
+  for (int nb = 256; nb >= 64; nb -= 16) {
+    if (pow2_only && (nb & (nb - 1))) continue;
     if (force && nb != force) continue;
+    if (!fits(nb)) continue;
     const long tiles = static_cast<long>(tiles_per_col_unit) * ((n_cols + nb - 1) / nb);
     const long waves = (tiles + num_sms - 1) / num_sms;
-    const double tt = static_cast<double>(waves) * nb * cost[k];
+    const double tt = static_cast<double>(waves) * (nb + 171.0);
     if (tt < best_t - 1e-9) {
       best_t = tt;
       best = nb;
@@ -557,12 +564,10 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   const uint32_t fixed = 1024 + static_cast<uint32_t>(G * cout) * 4 + 256;
   if (a.w_bytes + fixed >= kSmemLimit) return "conv_pp: weights do not fit in shared memory";
   const uint32_t budget = kSmemLimit - fixed - a.w_bytes;
-  int fits[3];
-  const int cands[3] = {256, 128, 64};
-  for (int k = 0; k < 3; ++k) {
-    const int R = round_up(8 + cands[k] + dr_max, 8);
-    fits[k] = (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
-  }
+  auto fits = [&](int nb) {  // two B stages at least, TMA box rows <= 256
+    const int R = round_up(8 + nb + dr_max, 8);
+    return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
+  };
   a.nb = pick_nb(a.P, n_cols, num_sms, fits);
   if (!a.nb) return "conv_pp: no column tile fits in shared memory";
   a.R = round_up(8 + a.nb + dr_max, 8);
@@ -574,7 +579,8 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   }
   a.nt_per_p = (n_cols + a.nb - 1) / a.nb;
   a.num_tiles = a.P * a.nt_per_p;
-  a.tmem_cols = static_cast<uint32_t>(2 * a.nb < 32 ? 32 : 2 * a.nb);
+  a.tmem_cols = 32;
+  while (a.tmem_cols < static_cast<uint32_t>(2 * a.nb)) a.tmem_cols <<= 1;  // allocation: a power of two
   a.wimg = wimg;
   a.bias = bias;
   a.bias_stride = static_cast<int>(bias_len(cout));
