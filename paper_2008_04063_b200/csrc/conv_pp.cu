@@ -495,6 +495,7 @@ static EncodeTiledFnPP get_encode_pp() {
 static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits) {
   static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
   static const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
+  static const double fixed_cols = getenv("HB_PP_NB_FIXED") ? atof(getenv("HB_PP_NB_FIXED")) : 171.0;
   int best = 0;
   double best_t = 1e30;
   for (int nb = 256; nb >= 64; nb -= 16) {
@@ -503,7 +504,7 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::f
     if (!fits(nb)) continue;
     const long tiles = static_cast<long>(tiles_per_col_unit) * ((n_cols + nb - 1) / nb);
     const long waves = (tiles + num_sms - 1) / num_sms;
-    const double tt = static_cast<double>(waves) * (nb + 171.0);
+    const double tt = static_cast<double>(waves) * (nb + fixed_cols);
     if (tt < best_t - 1e-9) {
       best_t = tt;
       best = nb;
