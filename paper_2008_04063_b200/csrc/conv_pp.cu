@@ -49,6 +49,7 @@
 // D[(p', c), n].  Other shortcuts (maxpool, wider phases) are read by the
 // epilogue.  A member's last conv writes no output: the epilogue folds
 // mean-pool . FC into one partial per (tile, column half, warp).
+#include <algorithm>
 #include <functional>
 
 #include "hb_kernels.cuh"
@@ -79,6 +80,28 @@ __device__ __forceinline__ PPTile pp_tile(const PPArgs& a, int tile) {
 // Shortcut row load (HB_PP_DBG & 64: L2-only ld.global.cg instead of the
 // read-only L1 path).
 __device__ __forceinline__ uint4 ldres_sel(const uint4* p, bool cg) { return cg ? __ldcg(p) : __ldg(p); }
+
+// This CTA's tiles: first, first + stride, ... < end.  Default: round robin
+// over every tile of the group.  member_split: the CTAs are partitioned
+// between the group's members in contiguous blocks, so a CTA never changes
+// weight image (the planner enables it when it costs no extra wave).
+struct CtaRange {
+  int first, stride, end;
+};
+__device__ __forceinline__ CtaRange cta_range(const PPArgs& a) {
+  CtaRange r{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), a.num_tiles};
+  if (a.member_split) {
+    const int grid = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+    int g = 0;
+    while (g + 1 < a.G && ((g + 1) * grid) / a.G <= c) ++g;
+    const int lo = (g * grid) / a.G, hi = ((g + 1) * grid) / a.G;
+    const int per_g = a.Pm * a.nt_per_p;
+    r.first = g * per_g + (c - lo);
+    r.stride = hi - lo;
+    r.end = (g + 1) * per_g;
+  }
+  return r;
+}
 
 __global__ void __launch_bounds__(kPPThreads, 1)
     conv_pp_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
@@ -113,8 +136,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     fence_barrier_init();
     // the first weight image (immutable, so before the dependency wait) goes out
     // right behind the barrier init: its latency hides the rest of the prologue
-    if (static_cast<int>(blockIdx.x) < a.num_tiles) {
-      const uint8_t* src = a.wimg + static_cast<size_t>(pp_tile(a, blockIdx.x).g) * a.w_stride;
+    const CtaRange cr = cta_range(a);
+    if (cr.first < cr.end) {
+      const uint8_t* src = a.wimg + static_cast<size_t>(pp_tile(a, cr.first).g) * a.w_stride;
       mbar_arrive_expect_tx(w_full, a.w_bytes);
       for (uint32_t off = 0; off < a.w_bytes; off += 32768u)
         bulk_load(sW + off, src + off, (a.w_bytes - off) < 32768u ? (a.w_bytes - off) : 32768u, w_full);
@@ -138,12 +162,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           bulk_load(sW + off, src + off, n, w_full);
         }
       };
-      int loaded_g = static_cast<int>(blockIdx.x) < a.num_tiles ? pp_tile(a, blockIdx.x).g : -1, reloads = 0;
+      const CtaRange cr = cta_range(a);
+      int loaded_g = cr.first < cr.end ? pp_tile(a, cr.first).g : -1, reloads = 0;
       pdl_wait();
       int st = 0;
       uint32_t sph = 0;
       const int planes_per_p = a.cin / 8;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      for (int tile = cr.first; tile < cr.end; tile += cr.stride) {
         const PPTile t = pp_tile(a, tile);
         if (t.g != loaded_g) {  // next member of the group: wait until the MMAs on the old weights retired
           mbar_wait(w_empty, static_cast<uint32_t>(reloads++) & 1u, 101);
@@ -180,10 +205,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     int acc = 0;
     uint32_t accph = 0;
     uint32_t wph = 0;
-    int cur_g = static_cast<int>(blockIdx.x) < a.num_tiles ? pp_tile(a, blockIdx.x).g : 0;
+    const CtaRange cr = cta_range(a);
+    int cur_g = cr.first < cr.end ? pp_tile(a, cr.first).g : 0;
     const bool prof = (a.dbg & 16) && a.prof && lane == 0;
     unsigned long long c_acc = 0, c_b = 0, c_start = prof ? clock64() : 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+    for (int tile = cr.first; tile < cr.end; tile += cr.stride) {
       const PPTile t = pp_tile(a, tile);
       if (t.g != cur_g) {
         wph ^= 1u;
@@ -238,8 +264,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       }
       if (elect_one()) mma_commit(&acc_full[acc]);
       __syncwarp();
-      const int nxt = tile + static_cast<int>(gridDim.x);
-      if (nxt < a.num_tiles && pp_tile(a, nxt).g != t.g) {  // the weights change after this tile
+      const int nxt = tile + cr.stride;
+      if (nxt < cr.end && pp_tile(a, nxt).g != t.g) {  // the weights change after this tile
         if (elect_one()) mma_commit(w_empty);
         __syncwarp();
       }
@@ -284,7 +310,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     unsigned long long e_wait = 0, e_work = 0, e_start = eprof ? clock64() : 0;
     int e_tiles = 0;
     pdl_wait();
-    for (int tile = blockIdx.x + eb * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+    const CtaRange cr = cta_range(a);
+    for (int tile = cr.first + eb * cr.stride; tile < cr.end; tile += 2 * cr.stride) {
       ++e_tiles;
       const PPTile t = pp_tile(a, tile);
       const float bias = s_bias[t.g * a.cout + c];
@@ -599,6 +626,16 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     return "conv_pp: maxpool shortcut shorter than the output";
   plan->smem_bytes = a.w_bytes + a.n_stages * a.stage_bytes + fixed;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
+  {  // member-partitioned CTAs when that costs no extra wave (HB_PP_SPLIT=0 disables)
+    static const int split_on = getenv("HB_PP_SPLIT") ? atoi(getenv("HB_PP_SPLIT")) : 1;
+    const int grid = plan->grid, per_g = a.Pm * a.nt_per_p;
+    int waves_split = 0;
+    for (int g = 0; g < G; ++g) {
+      const int n_g = ((g + 1) * grid) / G - (g * grid) / G;
+      waves_split = n_g < 1 ? 1 << 30 : std::max(waves_split, (per_g + n_g - 1) / n_g);
+    }
+    a.member_split = split_on && G > 1 && a.num_tiles > grid && waves_split <= (a.num_tiles + grid - 1) / grid;
+  }
 
   EncodeTiledFnPP enc = get_encode_pp();
   if (!enc) return "conv_pp: cuTensorMapEncodeTiled unavailable";

@@ -114,6 +114,7 @@ struct PPArgs {
   float* head_out;                 // [G][head_g_stride]: per patient head_mt = nt_per_p*8 partials
   size_t head_g_stride;
   int head_mt;
+  int member_split;                // CTAs partitioned by group member (no weight reloads inside a CTA)
   int dbg;                         // experiments only (HB_PP_DBG): 1 no epilogue math/stores, 2 no MMAs, 4 no B loads,
                                    // 16 role cycle counters into prof, 32 zero shortcut rows, 64 L2-only shortcut loads
   unsigned long long* prof;        // dbg & 16: per CTA [8]
