@@ -1076,8 +1076,10 @@ int hb_bench_conv_k(int P, int cin, int cout, int lin, int stride, int res_mode,
   CK(none, cudaMalloc(&din, in_b));
   CK(none, cudaMemset(din, 0, in_b));
   CK(none, cudaMalloc(&dout, out_b));
-  CK(none, cudaMalloc(&dres, in_b > out_b ? in_b : out_b));
-  CK(none, cudaMemset(dres, 0, in_b > out_b ? in_b : out_b));
+  // the shortcut tensor: x at the output length (identity) or twice the input length (maxpool)
+  const size_t res_b = std::max({in_b, out_b, static_cast<size_t>(P) * std::min(cin, cout) * plane_rows_max(2 * lin) * 2});
+  CK(none, cudaMalloc(&dres, res_b));
+  CK(none, cudaMemset(dres, 0, res_b));
   CK(none, cudaMalloc(&dw, wb));
   CK(none, cudaMemset(dw, 0, wb));
   CK(none, cudaMalloc(&db, nbias * 4));
