@@ -323,12 +323,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 #pragma unroll
       for (int k = 0; k < 8; ++k) fc8[k] = a.fc_w ? a.fc_w[static_cast<size_t>(t.g) * a.cout + g8 * 8 + k] : 0.f;
       // Shortcut rows of a chunk (2 positions per lane after the transpose;
-      // maxpool reads 2 rows each) are loaded one chunk ahead, the first
-      // before the accumulator wait.
-      uint4 raw[4];
+      // maxpool reads 2 rows each) are loaded two chunks ahead through two
+      // register sets (the chunk loop is unrolled by two so both stay in
+      // registers), the first two before the accumulator wait.
+      uint4 rawA[4], rawB[4];
       const bool cg = (a.dbg & 64) != 0;
       auto ldres = [&](const uint4* p) { return ldres_sel(p, cg); };
-      auto load_res = [&](int ch) {
+      auto load_res = [&](int ch, uint4 (&raw)[4]) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const int l = a.ph * (n_base + 16 * ch + 8 * b) + phase;
@@ -343,7 +344,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
           }
         }
       };
-      if (a.res_mode) load_res(c_lo);
+      if (a.res_mode) {
+        load_res(c_lo, rawA);
+        if (c_lo + 1 < c_hi) load_res(c_lo + 1, rawB);
+      }
       unsigned long long e0 = eprof ? clock64() : 0;
       mbar_wait(&acc_full[eb], accph, 120);
       tc_fence_after();
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         e0 = e1;
       }
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
-      for (int ch = c_lo; ch < c_hi; ++ch) {
+      auto chunk = [&](int ch, uint4 (&raw)[4]) {
         uint32_t r[16];
         tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 16), r);
         uint4 rv[2];
@@ -369,13 +373,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             rv[b] = a.res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
           }
         }
-        if (a.res_mode && ch + 1 < c_hi) load_res(ch + 1);
+        if (a.res_mode && ch + 2 < c_hi) load_res(ch + 2, raw);
         tmem_wait_ld();
         if (ch == c_hi - 1) {  // this warpgroup's columns drained
           tc_fence_before();
           mbar_arrive(&acc_empty[eb]);
         }
-        if (a.dbg & 1) continue;
+        if (a.dbg & 1) return;
         // (acc + bias) is rounded to fp16 before the transpose; the shortcut
         // add and ReLU run on half2 (two roundings instead of one: within one
         // fp16 ulp of the fp32 reference, tests/test_conv_pp_gpu.py).
@@ -412,6 +416,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             }
           }
         }
+      };
+      for (int ch = c_lo; ch < c_hi; ch += 2) {
+        chunk(ch, rawA);
+        if (ch + 1 < c_hi) chunk(ch + 1, rawB);
       }
       if (a.fc_w != nullptr) {  // one partial per (tile, epilogue warp), summed in fixed order by K5
 #pragma unroll
