@@ -44,3 +44,4 @@ for i in range(200):
     s = eng.submit(hin[i])
     eng.collect(s, out=out)
 print("submit+collect back to back (incl. device): %.1f us" % ((time.perf_counter() - t0) / 200 * 1e6))
+print("graph only again, after the loops (same thermal state): %.1f us" % (eng.time_tick(50) * 1e6))
