@@ -527,10 +527,16 @@ static EncodeTiledFnPP get_encode_pp() {
 // Widths between the powers of two trim the padding of awkward rows (L = 7500
 // gives 1875 / 938 / 469 columns: 240-wide tiles instead of 256 drop the
 // 9 % padded columns to 2 %).
-static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits) {
+static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits,
+                   bool maxpool_epi) {
   static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
   static const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
   static const double fixed_cols = getenv("HB_PP_NB_FIXED") ? atof(getenv("HB_PP_NB_FIXED")) : 171.0;
+  // maxpool shortcut in the epilogue at ph >= 4: the epilogue, not the MMA, sets
+  // the pace and narrower tiles overlap it better (tools/nb_sweep.py: 160-wide
+  // tiles 8-14 % faster on the 32-channel maxpool layers) - a smaller fixed term
+  static const double fixed_mp = getenv("HB_PP_NB_FIXED_MP") ? atof(getenv("HB_PP_NB_FIXED_MP")) : 60.0;
+  const double fixed = maxpool_epi ? fixed_mp : fixed_cols;
   int best = 0;
   double best_t = 1e30;
   for (int nb = 256; nb >= 64; nb -= 16) {
@@ -539,7 +545,7 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::f
     if (!fits(nb)) continue;
     const long tiles = static_cast<long>(tiles_per_col_unit) * ((n_cols + nb - 1) / nb);
     const long waves = (tiles + num_sms - 1) / num_sms;
-    const double tt = static_cast<double>(waves) * (nb + fixed_cols);
+    const double tt = static_cast<double>(waves) * (nb + fixed);
     if (tt < best_t - 1e-9) {
       best_t = tt;
       best = nb;
@@ -604,7 +610,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     const int R = round_up(8 + nb + dr_max, 8);
     return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
   };
-  a.nb = pick_nb(a.P, n_cols, num_sms, fits);
+  a.nb = pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4);
   if (!a.nb) return "conv_pp: no column tile fits in shared memory";
   a.R = round_up(8 + a.nb + dr_max, 8);
   a.stage_bytes = static_cast<uint32_t>(2 * a.Q * a.R * 16);
