@@ -139,6 +139,16 @@ int hb_last_windows(hb_ctx* ctx, float* raw, float* stats, void* stream);
 int hb_profile_tick(hb_ctx* ctx, void* stream, int cap, int* kinds, float* ms, double* flops, double* bytes);
 /* Algorithmic work of one tick: conv FLOPs and activation bytes (all selected members). */
 int hb_tick_work(const hb_ctx* ctx, double* flops, double* bytes);
+/* Diagnostics: the z-normalised fp16 windows [n_leads][P][window] (IEEE half bit
+ * patterns) that the members of the most recent tick consumed (K2's output). */
+int hb_last_normalized(hb_ctx* ctx, uint16_t* xn, void* stream);
+/* Host-only query of the frozen layer table the library serves (stem first,
+ * then conv1/conv2 of every block): per layer 9 ints
+ * {cin, cout, stride, lin, lout, pad_left, shortcut (0 none, 1 identity,
+ * 2 maxpool), shortcut channels, head}.  Returns the layer count (writes at
+ * most cap layers) or -HB_E_INVALID.  No device is touched; the CPU tests
+ * compare it with the Python table and the oracle's own restatement. */
+int hb_member_layers(int width, int depth, int window, int* out, int cap);
 
 /* ---------------------------------------------------------------- K6 sweep
  * Profiler sweep over a recorded cohort (replaces exhaustive_search's batched

@@ -59,6 +59,8 @@ _SIGS = {
     "hb_profile_tick": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int), _F, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]),
     "hb_tick_work": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "hb_last_normalized": (C.c_int, [_P, _P, _P]),
+    "hb_member_layers": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int]),
     "hb_sweep_auc": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,
                                C.POINTER(C.c_uint32), C.c_int, C.POINTER(C.c_double)]),
     "hb_cohort_create": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int8), C.c_int, C.c_int,

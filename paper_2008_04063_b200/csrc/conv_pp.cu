@@ -527,8 +527,14 @@ static EncodeTiledFnPP get_encode_pp() {
 // Widths between the powers of two trim the padding of awkward rows (L = 7500
 // gives 1875 / 938 / 469 columns: 240-wide tiles instead of 256 drop the
 // 9 % padded columns to 2 %).
+// The head layer (a member's last conv, fused mean-pool + FC) is the exception:
+// its tile width sets how the fp32 pooled sum is split into per-(tile, warp)
+// partials, so it is chosen from the layer shape alone (the same model with the
+// wave quantisation dropped, i.e. as if the batch were large).  A bed's logit
+// is then bit-identical whatever the batch size, shard or grid cap.  HB_PP_NB
+// forces a width wherever it fits (elsewhere the model chooses).
 static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits,
-                   bool maxpool_epi) {
+                   bool maxpool_epi, bool shape_only) {
   static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
   static const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
   static const double fixed_cols = getenv("HB_PP_NB_FIXED") ? atof(getenv("HB_PP_NB_FIXED")) : 171.0;
@@ -536,16 +542,17 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::f
   // the pace and narrower tiles overlap it better (tools/nb_sweep.py: 160-wide
   // tiles 8-14 % faster on the 32-channel maxpool layers) - a smaller fixed term
   static const double fixed_mp = getenv("HB_PP_NB_FIXED_MP") ? atof(getenv("HB_PP_NB_FIXED_MP")) : 60.0;
+  if (force >= 64 && force <= 256 && force % 16 == 0 && fits(force)) return force;
   const double fixed = maxpool_epi ? fixed_mp : fixed_cols;
   int best = 0;
   double best_t = 1e30;
   for (int nb = 256; nb >= 64; nb -= 16) {
     if (pow2_only && (nb & (nb - 1))) continue;
-    if (force && nb != force) continue;
     if (!fits(nb)) continue;
-    const long tiles = static_cast<long>(tiles_per_col_unit) * ((n_cols + nb - 1) / nb);
-    const long waves = (tiles + num_sms - 1) / num_sms;
-    const double tt = static_cast<double>(waves) * (nb + fixed);
+    const long col_tiles = (n_cols + nb - 1) / nb;
+    const long tiles = static_cast<long>(tiles_per_col_unit) * col_tiles;
+    const double waves = shape_only ? static_cast<double>(col_tiles) : static_cast<double>((tiles + num_sms - 1) / num_sms);
+    const double tt = waves * (nb + fixed);
     if (tt < best_t - 1e-9) {
       best_t = tt;
       best = nb;
@@ -610,7 +617,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     const int R = round_up(8 + nb + dr_max, 8);
     return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
   };
-  a.nb = pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4);
+  a.nb = pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4, fc_w != nullptr);
   if (!a.nb) return "conv_pp: no column tile fits in shared memory";
   a.R = round_up(8 + a.nb + dr_max, 8);
   a.stage_bytes = static_cast<uint32_t>(2 * a.Q * a.R * 16);

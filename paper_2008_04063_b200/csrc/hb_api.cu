@@ -173,6 +173,7 @@ struct hb_ctx {
   cudaGraphExec_t graph_io[2] = {nullptr, nullptr};
   cudaEvent_t io_done[2] = {nullptr, nullptr};
   bool io_busy[2] = {false, false};
+  int slot_M[2] = {0, 0};  // members of the tick submitted into each slot (its h_out layout)
   std::vector<LayerPlan> plans;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
@@ -636,6 +637,8 @@ int hb_add_member(hb_ctx* c, int idx, int lead, int width, int depth, const floa
   if (lead < 0 || lead >= c->leads)
     return fail(c, HB_E_CONFIG, "rates: no stream configured for lead " + std::to_string(lead));
   if (width < 8 || width % 8 || width > 128 || depth < 1) return fail(c, HB_E_INVALID, "unsupported width/depth");
+  if (c->io_busy[0] || c->io_busy[1])
+    return fail(c, HB_E_STATE, "a submitted tick is uncollected; collect it before registering members");
   cudaSetDevice(c->device);
   Member m;
   m.idx = idx;
@@ -713,6 +716,8 @@ int hb_set_selector(hb_ctx* c, const uint8_t* bits, int n) {
   }
   if (sel.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
   if (static_cast<int>(sel.size()) > kMaxMembers) return fail(c, HB_E_INVALID, "too many selected members");
+  if (sel != c->selected && (c->io_busy[0] || c->io_busy[1]))
+    return fail(c, HB_E_STATE, "a submitted tick is uncollected; collect it before changing the selector");
   if (sel != c->selected) {
     c->selected = sel;
     c->dirty = true;
@@ -784,9 +789,12 @@ int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool ov
   if (slot < 0 || slot > 1) return fail(c, HB_E_INVALID, "slot must be 0 or 1");
   cudaSetDevice(c->device);
   cudaStream_t st = pick(c, stream);
+  // the busy check comes first: rebuilding a selection frees both slots' pinned outputs
+  if (c->io_busy[slot]) return fail(c, HB_E_STATE, "slot " + std::to_string(slot) + " has an uncollected tick");
+  if (c->dirty && (c->io_busy[0] || c->io_busy[1]))
+    return fail(c, HB_E_STATE, "the selection changed while a submitted tick is uncollected; collect it first");
   const int rc = build_selection(c);
   if (rc) return rc;
-  if (c->io_busy[slot]) return fail(c, HB_E_STATE, "slot " + std::to_string(slot) + " has an uncollected tick");
   if (samples && overlap_h2d) {  // H2D on the copy stream into this slot's staging buffer: overlaps the tick in flight
     CK(c, cudaMemcpyAsync(c->staged_io[slot], samples, sizeof(float) * c->P * c->leads * c->hop,
                           cudaMemcpyHostToDevice, c->copy));
@@ -805,6 +813,7 @@ int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool ov
   CK(c, cudaEventRecord(c->io_done[slot], st));
   c->timed = true;
   c->io_busy[slot] = true;
+  c->slot_M[slot] = static_cast<int>(c->selected.size());
   return HB_OK;
 }
 
@@ -817,7 +826,8 @@ int hb_tick_collect(hb_ctx* c, int slot, float* member_logits, float* ens_prob, 
   cudaSetDevice(c->device);
   c->io_busy[slot] = false;
   CK(c, cudaEventSynchronize(c->io_done[slot]));
-  const size_t P = c->P, M = c->selected.size();
+  // the layout of the tick submitted into this slot, not of the selection now
+  const size_t P = c->P, M = static_cast<size_t>(c->slot_M[slot]);
   const float* h = c->h_out[slot];
   if (member_logits) std::memcpy(member_logits, h, sizeof(float) * P * M);
   if (ens_prob) std::memcpy(ens_prob, h + P * M, sizeof(float) * P);
@@ -958,6 +968,32 @@ int hb_tick_work(const hb_ctx* c, double* flops, double* bytes) {
   if (flops) *flops = f * c->P;
   if (bytes) *bytes = b * c->P;
   return HB_OK;
+}
+
+int hb_last_normalized(hb_ctx* c, uint16_t* xn, void* stream) {
+  if (!c || !xn) return fail(c, HB_E_INVALID, "null argument");
+  if (!c->xn) return fail(c, HB_E_STATE, "no selection built yet (tick first)");
+  cudaSetDevice(c->device);
+  cudaStream_t st = pick(c, stream);
+  // device layout [leads][P_pad][roundup(W, 8)] -> host [leads][P][W]
+  const size_t Wp = round_up(c->W, 8);
+  for (int lead = 0; lead < c->leads; ++lead)
+    CK(c, cudaMemcpy2DAsync(xn + static_cast<size_t>(lead) * c->P * c->W, sizeof(uint16_t) * c->W,
+                            c->xn + static_cast<size_t>(lead) * c->P_pad * Wp, sizeof(uint16_t) * Wp,
+                            sizeof(uint16_t) * c->W, c->P, cudaMemcpyDeviceToHost, st));
+  CK(c, cudaStreamSynchronize(st));
+  return HB_OK;
+}
+
+int hb_member_layers(int width, int depth, int window, int* out, int cap) {
+  if (width < 8 || width % 8 || depth < 1 || window < kTaps || cap < 0) return -HB_E_INVALID;
+  const std::vector<LayerSpec> v = member_layers(width, depth, window);
+  for (int i = 0; i < static_cast<int>(v.size()) && i < cap && out; ++i) {
+    const LayerSpec& L = v[i];
+    const int row[9] = {L.cin, L.cout, L.stride, L.lin, L.lout, L.pad, L.res_mode, L.res_c, L.head};
+    std::copy(row, row + 9, out + 9 * i);
+  }
+  return static_cast<int>(v.size());
 }
 
 // ----------------------------------------------------------------- test entry points

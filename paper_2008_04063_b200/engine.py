@@ -78,6 +78,7 @@ class EnsembleEngine:
         self._hb_submit = L.hb_tick_submit
         self._hb_collect = L.hb_tick_collect
         self._next_slot = 0
+        self._slot_ids: list = [None, None]  # member ids of the tick submitted into each slot
         self._out_ptrs = None  # (out, member_logits, ens_prob, ens_mean_logit addresses) of the last TickResult
         self._registered: set = set()
         to_register = range(zoo.n) if register == "all" else selector.indices()
@@ -127,8 +128,9 @@ class EnsembleEngine:
         with self._lock:
             _lib.check(_lib.lib().hb_ingest(self._h, _lib.fptr(a), a.shape[2], None), self._h)
 
-    def _ptrs_of(self, out: TickResult) -> tuple:
-        for arr, shape in ((out.member_logits, (self.patients, self.selector.popcount)),
+    def _ptrs_of(self, out: TickResult, M: int | None = None) -> tuple:
+        M = self.selector.popcount if M is None else M
+        for arr, shape in ((out.member_logits, (self.patients, M)),
                            (out.ens_prob, (self.patients,)), (out.ens_mean_logit, (self.patients,))):
             if arr.dtype != np.float32 or not arr.flags.c_contiguous or arr.shape != shape:
                 raise ValueError(f"output buffers must be C-contiguous float32 of shape {shape}")
@@ -172,24 +174,27 @@ class EnsembleEngine:
         slot = self._next_slot
         with self._lock:
             rc = self._hb_submit(self._h, a.ctypes.data, slot, None)
-        if rc:
-            _lib.check(rc, self._h)
+            if rc:
+                _lib.check(rc, self._h)
+            self._slot_ids[slot] = self.member_ids
         self._next_slot = slot ^ 1
         return slot
 
     def collect(self, slot: int, out: TickResult | None = None) -> TickResult:
-        """Pipelined tick, second half: wait for the tick submitted into ``slot`` and return its outputs."""
+        """Pipelined tick, second half: wait for the tick submitted into ``slot`` and return its outputs
+        (labelled with the members that tick was submitted with)."""
+        ids = self._slot_ids[slot] if slot in (0, 1) and self._slot_ids[slot] is not None else self.member_ids
         if out is None:
-            M = self.selector.popcount
-            out = TickResult(self.member_ids, np.empty((self.patients, M), np.float32),
+            out = TickResult(ids, np.empty((self.patients, len(ids)), np.float32),
                              np.empty(self.patients, np.float32), np.empty(self.patients, np.float32))
         cached = self._out_ptrs
         if cached is None or cached[0] is not out:
-            cached = self._out_ptrs = self._ptrs_of(out)
+            cached = self._out_ptrs = self._ptrs_of(out, len(ids))
         with self._lock:
             rc = self._hb_collect(self._h, slot, cached[1], cached[2], cached[3])
-        if rc:
-            _lib.check(rc, self._h)
+            if rc:
+                _lib.check(rc, self._h)
+            self._slot_ids[slot] = None
         return out
 
     def stage_device(self, dev_ptr: int, stream: int | None = None) -> None:
@@ -211,6 +216,12 @@ class EnsembleEngine:
         stats = np.empty((self.patients, self.leads, 2), np.float32)
         _lib.check(_lib.lib().hb_last_windows(self._h, _lib.fptr(raw), _lib.fptr(stats), None), self._h)
         return raw, stats
+
+    def last_normalized(self) -> np.ndarray:
+        """The z-normalised fp16 windows [leads, P, W] the latest tick's members consumed."""
+        out = np.empty((self.leads, self.patients, self.window), np.float16)
+        _lib.check(_lib.lib().hb_last_normalized(self._h, C.c_void_p(out.ctypes.data), None), self._h)
+        return out
 
     def profile_tick(self, stream: int | None = None, cap: int = 4096):
         """Per-launch (kind, ms, flops, bytes) of one eagerly launched tick (advances the stream)."""

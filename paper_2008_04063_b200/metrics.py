@@ -89,3 +89,22 @@ def f1_accuracy(labels, scores, threshold: float = 0.5) -> tuple[float, float]:
     wrong = int(np.sum(pred != actual))
     denom = 2 * tp + wrong
     return ((2 * tp / denom) if denom else 0.0), float(np.mean(pred == actual))
+
+
+def sweep_auc(labels, score_matrix, selectors, device: int = 0) -> np.ndarray:
+    """AUC of the ensemble mean of every selector, one shot through the C-ABI's `hb_sweep_auc`
+    (the batched accuracy pass of `exhaustive_search`, composer.py:614-619): `selectors` are
+    ints whose bit k selects column k (LSB = model 0, composer.py:616), n <= 32 columns."""
+    import ctypes as C
+
+    from . import _lib
+    lab, _ = validate(labels, np.zeros(len(labels)))
+    mat = np.ascontiguousarray(score_matrix, dtype=np.float64)
+    if mat.ndim != 2 or mat.shape[0] != lab.size:
+        raise ValueError("score_matrix must be (n_samples, n_columns)")
+    sel = np.ascontiguousarray(selectors, dtype=np.uint32)
+    out = np.empty(sel.size, np.float64)
+    rc = _lib.lib().hb_sweep_auc(device, _lib.dptr(mat), lab.ctypes.data_as(C.POINTER(C.c_int8)), mat.shape[0],
+                                 mat.shape[1], sel.ctypes.data_as(C.POINTER(C.c_uint32)), sel.size, _lib.dptr(out))
+    _lib.check(rc, None, "hb_cohort_last_error")
+    return out

@@ -5,7 +5,9 @@ Two ways to spread the tick:
 * **Patient sharding** (`PatientShardedEngine`): contiguous bed ranges per
   rank; every rank owns its beds' rings, all selected members' weights and its
   own tick graph.  Beds are independent, so there is NO collective on the data
-  path; per-bed results equal the 1-GPU results bit for bit.  Results are
+  path; per-bed results equal the 1-GPU results bit for bit at any shard size
+  (every kernel is per bed, and the fused head's partial-sum grouping is fixed
+  by the layer shape, not by the batch: `pick_nb` in csrc/conv_pp.cu).  Results are
   gathered to rank 0 only when the caller asks (`gather`).
 * **Member sharding** (`MemberShardedEngine`, config c5): the selected members
   are FLOP-balanced over ranks (`member_bins`); every rank ingests every
@@ -127,10 +129,20 @@ class PatientShardedEngine:
 
 
 class MemberShardedEngine:
-    """This rank's FLOP-balanced share of the members; one SUM reduce per tick."""
+    """This rank's FLOP-balanced share of the members; one SUM reduce per tick.
+
+    Serving path per tick, all stream-ordered on one CUDA stream with a single
+    host synchronisation at the end: the hop of every bed is copied into a
+    pinned staging buffer and sent H2D in-stream, the tick graph runs this
+    rank's members, the per-bed partial sums [2, P] are reduced IN PLACE
+    (NCCL over NVLink; the aggregate kernel rewrites them every tick, so no
+    copy is needed), and rank 0's finalize kernel divides by the total
+    popcount and its D2H lands in pinned host buffers."""
 
     def __init__(self, zoo: ModelZoo, selector: Selector, patients: int, rank: int, world: int, group=None,
                  **engine_kw):
+        import torch
+
         from .engine import EnsembleEngine
         self.rank, self.world, self.group = rank, world, group
         self.bins = member_bins(zoo, selector, world)
@@ -138,28 +150,72 @@ class MemberShardedEngine:
         self.patients = patients
         mine = Selector.from_indices(zoo.n, self.bins[rank])
         self.engine = EnsembleEngine(zoo, mine, patients, **engine_kw)
-        import torch
         # a real (non-legacy) stream: the library treats handle 0 as "its own
         # stream", which does not order with torch's legacy default stream
         self.stream = torch.cuda.Stream()
+        e = self.engine
+        self._stage = torch.empty((patients, e.leads, e.hop), dtype=torch.float32, pin_memory=True)
+        self._stage_np = self._stage.numpy()
+        self._prob = torch.empty(patients, dtype=torch.float32, device="cuda")
+        self._logit = torch.empty(patients, dtype=torch.float32, device="cuda")
+        self._h_out = torch.empty((2, patients), dtype=torch.float32, pin_memory=True)
+        self._sums = None
 
     def _sums_tensor(self):
         import torch
-        ptr = C.c_void_p()
+        ptr = C.c_void_p()   # (valid once a tick built the selection; re-read: a rebuild moves it)
         _lib.check(_lib.lib().hb_device_sums(self.engine._h, C.byref(ptr)), self.engine._h)
-        return torch.as_tensor(CudaView(ptr.value, (2, self.patients)), device="cuda")
+        if self._sums is None or self._sums.data_ptr() != ptr.value:
+            self._sums = torch.as_tensor(CudaView(ptr.value, (2, self.patients)), device="cuda")
+        return self._sums
+
+    def reduce_device(self, stream=None) -> None:
+        """After this rank's tick on `stream`: the in-place NCCL reduce of the partial sums to rank 0 and
+        (rank 0) the finalize kernel into device buffers; stream-ordered, no host synchronisation."""
+        import torch
+        import torch.distributed as dist
+        stream = stream or self.stream
+        with torch.cuda.stream(stream):
+            sums = self._sums_tensor()
+            dist.reduce(sums, dst=0, op=dist.ReduceOp.SUM, group=self.group)
+            if dist.get_rank(self.group) == 0:
+                _lib.check(_lib.lib().hb_finalize_sums(C.c_void_p(sums.data_ptr()), self.patients, int(self.m_total),
+                                                       C.c_void_p(self._prob.data_ptr()),
+                                                       C.c_void_p(self._logit.data_ptr()),
+                                                       C.c_void_p(stream.cuda_stream)))
+
+    def finished_outputs(self):
+        """(prob, mean_logit) numpy of the last reduced tick on rank 0 (synchronises), else (None, None)."""
+        import torch.distributed as dist
+        self.stream.synchronize()
+        import torch
+        torch.cuda.synchronize()
+        if dist.get_rank(self.group) != 0:
+            return None, None
+        return self._prob.cpu().numpy(), self._logit.cpu().numpy()
 
     def tick(self, samples_all: np.ndarray):
-        """Every rank passes ALL beds' samples [P, leads, hop]; rank 0 gets (prob, logit) device tensors."""
+        """Every rank passes ALL beds' samples [P, leads, hop]; rank 0 gets (prob, mean_logit) as CPU tensors,
+        the other ranks None."""
         import torch
-        a = np.ascontiguousarray(samples_all, dtype=np.float32)
-        with torch.cuda.stream(self.stream):
-            staged = torch.from_numpy(a).cuda(non_blocking=False)
-            self.engine.stage_device(staged.data_ptr(), self.stream.cuda_stream)
-            self.engine.tick_device(self.stream.cuda_stream)
-            out = combine_member_sums(self._sums_tensor(), self.m_total, self.group)
-        self.stream.synchronize()
-        return out
+        import torch.distributed as dist
+        e = self.engine
+        np.copyto(self._stage_np, samples_all, casting="same_kind")
+        st = self.stream
+        with e._lock:
+            rc = _lib.lib().hb_tick(e._h, C.c_void_p(self._stage_np.ctypes.data), None, None, None,
+                                    C.c_void_p(st.cuda_stream))
+        if rc:
+            _lib.check(rc, e._h)
+        self.reduce_device(st)
+        root = dist.get_rank(self.group) == 0
+        if root:
+            with torch.cuda.stream(st):
+                self._h_out[0].copy_(self._prob, non_blocking=True)
+                self._h_out[1].copy_(self._logit, non_blocking=True)
+        st.synchronize()
+        return (self._h_out[0].clone(), self._h_out[1].clone()) if root else None
 
     def close(self):
+        self._sums = None
         self.engine.close()

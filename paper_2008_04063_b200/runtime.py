@@ -273,6 +273,58 @@ def _run_ticks(zoo, b, patients, window_s, duration_s, agg_overhead_s, stagger, 
     return out
 
 
+def run_simulation_wallclock(zoo: ModelZoo, b: Selector, executor: ExecutorModel, patients: int, rates: dict,
+                             window_s: float, duration_s: float, seed: int = 0, correlation: float = 0.5, *,
+                             hop: int | None = None, device: int = 0, speedup: float = 1.0, source=None) -> list:
+    """Wall-clock mode with the reference's signature (`runtime.py:321-396`), served by the device.
+
+    The reference runs one ingest thread per patient feeding per-sample
+    `Aggregator`s, emits a query when every needed modality flushed window k,
+    and lets `executor.n_slots` workers `sleep(service_time)`.  Here a sensor
+    thread delivers one frame per hop (every bed's and lead's newest samples,
+    tumbling windows by default: hop = rate * window_s, exactly the
+    Aggregator's windows) and one device worker scores each frame in ONE
+    `EnsembleEngine.tick` (`serving.ServingLoop`).  The trace schema, ordering
+    (query id = tick * patients + bed) and timestamps (seconds since start;
+    `t_ingest` = the window's start) follow the reference.  `model_scores` are
+    the members' real logits and `ensemble_score` the mean latent
+    (`runtime.py:136`), not binormal draws, so `correlation` is accepted for
+    signature compatibility only; the measured tick replaces `service_time`,
+    so `executor` only validates.  `seed` seeds the synthetic ECG streams
+    (`source(start, count) -> [P, leads, count]` overrides them; the
+    reference's own generator sends 0.0, `synth.zero_stream`).  `speedup`
+    compresses time (1.0 = real time, as the reference).
+    """
+    from . import synth
+    from .engine import EnsembleEngine
+    from .serving import ServingLoop
+    check_modalities(zoo, b, rates)
+    if not isinstance(executor, ExecutorModel):
+        raise ConfigurationError("executor must be an ExecutorModel")
+    if window_s <= 0 or duration_s < window_s:
+        raise ConfigurationError("window_s must be positive and duration_s >= window_s")
+    if patients < 1:
+        raise ConfigurationError("patients must be >= 1")
+    for modality, rate in rates.items():
+        samples_per_window(modality, rate, window_s)
+    fs = set(float(r) for r in rates.values())
+    if len(fs) != 1:
+        raise ConfigurationError("rates: the device engine needs one common sampling rate for all leads")
+    fs_v = fs.pop()
+    W = samples_per_window("*", fs_v, window_s)
+    hop = W if hop is None else int(hop)
+    leads = 1 + max(modality_lead(m) for m in rates)
+    if source is None:
+        def source(start, count, _p=patients, _l=leads):
+            return synth.ecg_block(seed, _p, _l, start, count)
+    # ticks whose window ends by duration_s (the reference flushes floor(duration * rate) samples)
+    n_ticks = (int(math.floor(duration_s * fs_v + 1e-9)) - W) // hop + 1
+    with EnsembleEngine(zoo, b, patients, leads=leads, fs=int(round(fs_v)), window_s=window_s, hop=hop,
+                        seed=0, device=device) as eng:
+        traces = ServingLoop(eng, source, speedup=speedup).run(n_ticks)
+    return sorted(traces, key=lambda t: t.query_id)
+
+
 def e2e_percentiles(traces: list) -> dict:
     """Nearest-rank p50/p95/p99 of done - enqueue ("query") and done - ingest ("capture")."""
     if not traces:

@@ -81,3 +81,9 @@ def test_config_errors_map_to_configuration_error():
     h = C.c_void_p()
     with pytest.raises(errors.ConfigurationError, match="hop"):
         _lib.check(L.hb_create(0, C.byref(cfg), C.byref(h)))
+
+
+def test_one_shot_sweep_rejects_wide_cohorts_before_device_work():
+    from paper_2008_04063_b200 import metrics
+    with pytest.raises(ValueError, match="n must be <= 32"):
+        metrics.sweep_auc(np.array([0, 1, 0, 1]), np.zeros((4, 33)), [1])

@@ -10,8 +10,8 @@ Bars (BASELINE.json north_star):
 import numpy as np
 import pytest
 
-from oracle import cnn, windows
-from paper_2008_04063_b200 import arch, synth
+from oracle import cnn, cpu_path, windows
+from paper_2008_04063_b200 import synth
 from paper_2008_04063_b200.zoo import Selector, holmes_zoo
 
 pytestmark = pytest.mark.gpu
@@ -29,16 +29,7 @@ def _streams(P, n, seed=0, zero_patient=None):
 
 
 def _oracle_tick(zoo, sel, streams, end, W=7500, seed=0):
-    P = streams.shape[0]
-    logits = []
-    for i in sel.indices():
-        prof = zoo.profiles[i]
-        win = np.stack([windows.sliding_window(streams[p, prof.lead], end, W) for p in range(P)])
-        params = arch.member_params(prof.width, prof.depth, seed, prof.id)
-        logits.append(cnn.member_forward(cnn.znorm(win), params, prof.width, prof.depth))
-    ml = np.stack(logits, axis=1)
-    prob, mean_logit = cnn.ensemble(ml)
-    return ml, prob, mean_logit
+    return cpu_path.cpu_tick(zoo, sel, streams, end, W, seed)
 
 
 def _compare(res, ml, prob, mean_logit):
@@ -221,3 +212,27 @@ def test_many_ticks_across_ring_wraps():
                     for lead in range(3):
                         assert np.array_equal(raw[p, lead], windows.sliding_window(streams[p, lead], end, W)), k
         _compare(res, *_oracle_tick(zoo, sel, streams, end))
+
+
+def test_selector_change_refused_while_a_tick_is_uncollected():
+    """a submitted tick keeps its own member layout.  Changing the selector (or
+    registering a member) while a slot holds an uncollected tick is refused (HB_E_STATE ->
+    RuntimeError) instead of freeing that slot's pinned outputs; after collect it works."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    P, W, hop = 3, 7500, 250
+    streams = _streams(P, W + hop, seed=9)
+    sel_a = Selector.from_indices(60, [0])
+    sel_b = Selector.from_indices(60, [0, 21, 40])
+    with EnsembleEngine(zoo, sel_a, P, hop=hop) as eng:
+        eng.ingest(streams[:, :, : W - hop])
+        slot = eng.submit(np.ascontiguousarray(streams[:, :, W - hop:W]))
+        with pytest.raises(RuntimeError, match="uncollected"):
+            eng.set_selector(sel_b)
+        res = eng.collect(slot)
+        assert res.member_ids == ("ecg-i-w8-d2",) and res.member_logits.shape == (P, 1)
+        _compare(res, *_oracle_tick(zoo, sel_a, streams, W))
+        eng.set_selector(sel_b)
+        res = eng.tick(np.ascontiguousarray(streams[:, :, W:W + hop]))
+        assert res.member_logits.shape == (P, 3)
+        _compare(res, *_oracle_tick(zoo, sel_b, streams, W + hop))

@@ -1,0 +1,162 @@
+"""Oracle parity at the configurations the benchmark times (VERDICT r1 lead item).
+
+The benchmark's c2 tick (4 members, 64 beds) and the north-star 1024-bed tick
+run K4b's multi-wave paths — persistent CTAs looping over several tiles, the
+second TMEM accumulator and its epilogue warpgroups, member-partitioned CTAs,
+mid-CTA weight reloads, 160/240-wide column tiles — that small-P tests never
+reach.  Every test here compares the device tick through the C-ABI with the
+CPU fp32 oracle (`oracle/cpu_path.cpu_tick`, PyTorch fp32, the oracle's own
+layer table) on identical synthetic streams:
+
+  * raw window samples: bit-exact (`Aggregator` semantics, runtime.py:98-115);
+  * z-normalised fp16 windows: within 1 fp16 ulp of the fp64 oracle value;
+  * member / ensemble probabilities: |dev - oracle| <= 1e-3 (north star);
+  * logits: <= 2e-2 (sigmoid saturation cannot hide an error).
+
+Configs: BASELINE.json configs c1 (1 member, 1 bed), c2 (4 members, 64 beds,
+every bed, 3 sliding ticks), north-star scale (1024 beds, 64 sampled beds),
+c3 (60-member zoo, 100 beds, sampled beds), plus the multi-tile K4b paths
+forced at small P through the planner's knobs.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import cnn, cpu_path, windows
+from paper_2008_04063_b200 import synth
+from paper_2008_04063_b200.zoo import Selector, holmes_zoo
+
+pytestmark = pytest.mark.gpu
+
+PROB_TOL = 1e-3
+LOGIT_TOL = 2e-2
+W = 7500
+C2 = [10, 13, 30, 50]   # ecg-i-w32-d8, ecg-i-w64-d4, ecg-ii-w32-d8, ecg-iii-w32-d8
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _compare(got_ml, got_prob, got_ml_mean, ml, prob, mean_logit):
+    d_logit = float(np.abs(got_ml - ml).max())
+    d_mprob = float(np.abs(cnn.sigmoid(got_ml) - cnn.sigmoid(ml)).max())
+    d_prob = float(np.abs(got_prob - prob).max())
+    d_mean = float(np.abs(got_ml_mean - mean_logit).max())
+    assert d_logit <= LOGIT_TOL and d_mprob <= PROB_TOL and d_prob <= PROB_TOL and d_mean <= LOGIT_TOL, \
+        (d_logit, d_mprob, d_prob, d_mean)
+    return d_logit, d_prob
+
+
+XN_FLOOR = 1e-6
+
+
+def _check_xn(xn, streams, end, beds, zoo_leads=3):
+    """Device z-normalised windows vs the fp64 oracle: within one fp16 ulp at the oracle value's
+    magnitude, or XN_FLOOR absolute where that ulp is smaller (|z| < ~1e-3: the device's fp32
+    mean/std carry ~1e-7 of rounding that a subnormal-range fp16 ulp cannot absorb)."""
+    for lead in range(zoo_leads):
+        win = np.stack([windows.sliding_window(streams[p, lead], end, W) for p in beds]).astype(np.float64)
+        mean = win.mean(axis=-1, keepdims=True)
+        ref = (win - mean) / np.maximum(win.std(axis=-1, keepdims=True), 1e-6)
+        dev = xn[lead, beds].astype(np.float64)
+        ulp = np.maximum(np.spacing(np.abs(ref).astype(np.float16)).astype(np.float64), XN_FLOOR)
+        bad = np.abs(dev - ref) > ulp
+        assert not bad.any(), (lead, int(bad.sum()), float(np.abs(dev - ref).max()))
+
+
+def _run(sel, P, hop, ticks, seed, check_beds, zero_bed=None, check_every_tick=True, xn_check=True):
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    if zero_bed is not None:
+        streams[zero_bed] = 0.0          # the reference's own wall-clock signal (runtime.py:358)
+    worst = (0.0, 0.0)
+    with EnsembleEngine(zoo, sel, P, hop=hop, keep_windows=True) as eng:
+        eng.ingest(streams[:, :, :W - hop])
+        for k in range(ticks):
+            end = W + k * hop
+            res = eng.tick(streams[:, :, end - hop:end])
+            if not check_every_tick and k != ticks - 1:
+                continue
+            raw, stats = eng.last_windows()
+            for p in check_beds:
+                for lead in range(3):
+                    assert np.array_equal(raw[p, lead], windows.sliding_window(streams[p, lead], end, W)), (k, p)
+            if zero_bed is not None:
+                assert np.all(stats[zero_bed, :, 1] == 0.0)
+            if xn_check:
+                _check_xn(eng.last_normalized(), streams, end, check_beds)
+            ml, prob, mlog = cpu_path.cpu_tick(zoo, sel, streams, end, beds=check_beds)
+            d = _compare(res.member_logits[check_beds], res.ens_prob[check_beds], res.ens_mean_logit[check_beds],
+                         ml, prob, mlog)
+            worst = tuple(max(a, b) for a, b in zip(worst, d))
+    return worst
+
+
+def test_c1_one_member_one_bed():
+    """BASELINE c1: ecg-i-w32-d8, 1 bed, 1 s sliding ticks (the config the CPU reference runs)."""
+    _run(Selector.from_indices(60, [10]), 1, 250, 4, 0, [0])
+
+
+def test_c2_64_beds_every_bed_three_ticks():
+    """BASELINE c2 exactly as bench.py times it: 4 members, 64 beds, hop 250, every bed, 3 ticks."""
+    _run(Selector.from_indices(60, C2), 64, 250, 3, 0, list(range(64)), zero_bed=17)
+
+
+def test_north_star_1024_beds_sampled():
+    """The north-star scale: 1024 beds; 64 beds spread over the range (first, last, and
+    the chunk/tile boundaries in between) against the oracle, 2 ticks."""
+    beds = sorted(set(np.linspace(0, 1023, 62).astype(int).tolist()) | {511, 512})
+    _run(Selector.from_indices(60, C2), 1024, 250, 2, 1, beds, zero_bed=511, check_every_tick=False)
+
+
+def test_c3_full_zoo_100_beds_sampled():
+    """BASELINE c3: the whole 60-member zoo over 100 beds (K4 wide layers, streamed weights,
+    multi-N-tile heads), 5 sampled beds against the oracle."""
+    _run(Selector.ones(60), 100, 250, 1, 2, [0, 33, 50, 71, 99], xn_check=True)
+
+
+@pytest.mark.parametrize("lane_sms", ["3", "4", "6", "9"])
+def test_k4b_multi_tile_paths_forced(monkeypatch, lane_sms):
+    """Cap every conv grid at a few CTAs (HB_LANE_SMS) so that at 5 beds each persistent CTA
+    loops over many tiles: both TMEM accumulators and all four epilogue warpgroups, and either
+    member-partitioned CTAs (6, 9: the grid splits evenly over the 3-member group) or round-robin
+    CTAs that reload a different member's weight image mid-layer (3, 4)."""
+    monkeypatch.setenv("HB_LANE_SMS", ",".join([lane_sms] * 4))
+    _run(Selector.from_indices(60, C2), 5, 250, 2, 3, list(range(5)), xn_check=False)
+
+
+def test_k4b_group_caps(monkeypatch):
+    """HB_MAX_GROUP=2: the three w32 members split into a 2-group and a 1-group (other lanes,
+    other tile plans)."""
+    monkeypatch.setenv("HB_MAX_GROUP", "2")
+    _run(Selector.from_indices(60, C2), 7, 250, 1, 4, list(range(7)), xn_check=False)
+
+
+STATIC_KNOBS = [
+    {"HB_PP_NB": "64"},                       # narrowest column tiles: most tiles per CTA
+    {"HB_PP_NB": "256"},                      # widest tiles
+    {"HB_PP_NB": "160", "HB_PP_SPLIT": "0"},  # 160-wide tiles, round-robin CTAs
+    {"HB_PP_SPLIT": "0", "HB_LANE_SMS": "5,5,5,5"},
+    {"HB_PP_STAGES": "2"},                    # shallowest B pipeline
+    {"HB_PP_RES_EPI": "1"},                   # identity shortcut in the epilogue instead of MMAs
+    {"HB_WIN": "1"},                          # shared-memory window kernel
+]
+
+
+@pytest.mark.parametrize("env", STATIC_KNOBS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_k4b_planner_variants_match_oracle(tmp_path, env):
+    """Planner knobs read once per process: run the tick in a subprocess and check its outputs
+    against the oracle (64 beds, c2 — the benchmark's shape)."""
+    P, hop, ticks, seed = 64, 250, 2, 5
+    out = tmp_path / "tick.npz"
+    e = dict(os.environ, **env)
+    subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop), str(ticks),
+                    str(seed), ",".join(map(str, C2))], check=True, env=e, timeout=600)
+    got = np.load(out)
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = list(range(0, 64, 3))
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, C2), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)

@@ -76,14 +76,49 @@ def test_record_cohort_then_sweep():
 
 
 def test_measured_latency_profiler():
+    """The measured f_l times the candidate's real grouped tick: a 3-member ensemble of one
+    architecture costs far less than three separate ticks (grouped into one launch per layer),
+    measurements are cached per architecture multiset (leads do not matter), and mode="sum"
+    (the cheap additive estimate) is an upper bound."""
     zoo = holmes_zoo()
     sysc = latency.SystemConfig(n_slots=1, patients=16)
     mp = latency.MeasuredLatencyProfiler(zoo, sysc, reps=3)
-    t1 = mp.tick_seconds(Selector.from_indices(60, [10]))
-    t2 = mp.tick_seconds(Selector.from_indices(60, [10, 13]))
-    assert 0 < t1 < t2 < 0.2
-    rep = mp.report(Selector.from_indices(60, [10, 13]))
-    assert rep.feasible and rep.total_s < 0.2
+    try:
+        t1 = mp.tick_seconds(Selector.from_indices(60, [10]))
+        t2 = mp.tick_seconds(Selector.from_indices(60, [10, 13]))
+        t3 = mp.tick_seconds(Selector.from_indices(60, [10, 30, 50]))      # three w32-d8, one per lead
+        assert 0 < t1 < t2 < 0.2 and t1 < t3 < 2.5 * t1
+        n = mp.measurements()
+        assert mp.tick_seconds(Selector.from_indices(60, [30])) == t1     # same architecture, other lead
+        assert mp.measurements() == n
+        rep = mp.report(Selector.from_indices(60, [10, 13]))
+        assert rep.feasible and rep.total_s < 0.2
+    finally:
+        mp.close()
+    ms = latency.MeasuredLatencyProfiler(zoo, sysc, reps=3, mode="sum")
+    try:
+        assert ms.tick_seconds(Selector.from_indices(60, [10, 30, 50])) >= 0.9 * t3
+    finally:
+        ms.close()
+
+
+def test_exhaustive_search_with_measured_latency_profiler():
+    """SURVEY §8f row 1 end to end: composer.exhaustive_search over the n = 10 c4 cohort with the
+    device-measured f_l (every candidate's real tick at 64 beds) picks a feasible ensemble under
+    the paper's 200 ms budget, and its objective matches a re-evaluation of that selector."""
+    import os
+    from paper_2008_04063_b200 import zoo as hz
+    z10 = hz.load_zoo(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "zoo_10.json"))
+    coh = cohort.synthesize_cohort(z10, 2000, 2000, 0.5, 0)
+    sysc = latency.SystemConfig(n_slots=1, patients=64)
+    mp = latency.MeasuredLatencyProfiler(z10, sysc, reps=3)
+    try:
+        res = composer.exhaustive_search(z10, coh, mp, budget_s=0.2)
+        assert res.feasible and res.best_latency_s < 0.2
+        assert res.best_accuracy == composer.make_accuracy_profiler(coh)(res.best)
+        assert mp.measurements() <= 1023
+    finally:
+        mp.close()
 
 
 def test_serving_loop_realtime():
@@ -145,3 +180,41 @@ def test_device_arrival_curve_bit_identical(patients, jitter):
     b = latency.build_arrival_curve(tr, backend="device")
     assert np.array_equal(a.dts, b.dts) and np.array_equal(a.counts, b.counts)
     assert a.n_events == b.n_events and a.span_s == b.span_s
+
+
+@pytest.mark.parametrize("beds", [16, 1024, 4100, 8192])
+def test_device_arrival_curve_matches_reference_golden(beds):
+    """K7 against the REFERENCE's own curves (tests/golden/curves.npz, make_golden.py): the exact
+    branch and the binned branch (4100 beds = 8200 events, 8192 beds = 16 384 events)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "curves.npz"))
+    ts = latency.profiling_trace(latency.SystemConfig(patients=beds), seed=7)
+    a = latency.build_arrival_curve(ts, backend="device")
+    assert np.array_equal(a.dts, g[f"b{beds}_dts"]) and np.array_equal(a.counts, g[f"b{beds}_counts"])
+
+
+def test_run_simulation_wallclock_drop_in_signature():
+    """`run_simulation_wallclock(zoo, b, executor, patients, rates, window_s, duration_s, seed,
+    correlation)` with the reference's signature (runtime.py:321-396): one trace per (bed, window),
+    tumbling windows (= the reference Aggregator's), ordered timestamps, query ids in (window, bed)
+    order, and scores = the members' real logits on window k (oracle-checked).  Time runs 30x."""
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [10, 30])          # leads I and II
+    P, speed, seed = 4, 30.0, 3
+    ex = latency.ExecutorModel(n_slots=2)
+    tr = runtime.run_simulation_wallclock(zoo, sel, ex, P, RATES, 30.0, 90.0, seed, 0.5, speedup=speed)
+    assert len(tr) == 3 * P and [t.query_id for t in tr] == list(range(3 * P))
+    for t in tr:
+        assert t.t_ingest <= t.t_enqueue <= t.t_dequeue <= t.t_done
+        assert set(t.model_scores) == {"ecg-i-w32-d8", "ecg-ii-w32-d8"}
+    assert [round(tr[k * P].t_ingest * speed, 6) for k in range(3)] == [0.0, 30.0, 60.0]
+    streams = synth.ecg_block(seed, P, 3, 0, 3 * 7500)
+    for k in range(3):
+        ml, _, mlog = cpu_path.cpu_tick(zoo, sel, streams, (k + 1) * 7500)
+        got = np.array([[tr[k * P + p].model_scores[zoo.profiles[i].id] for i in sel.indices()] for p in range(P)])
+        assert np.abs(got - ml).max() <= 2e-2
+        assert np.abs(np.array([tr[k * P + p].ensemble_score for p in range(P)]) - mlog).max() <= 2e-2
+    pc = runtime.e2e_percentiles(tr)
+    assert pc["query"]["p99"] < 0.2
+    with pytest.raises(runtime.ConfigurationError):
+        runtime.run_simulation_wallclock(zoo, sel, ex, P, {"ECG-I": 250.0}, 30.0, 90.0)

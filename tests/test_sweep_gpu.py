@@ -117,3 +117,30 @@ def test_sweep_errors():
     with pytest.raises(ValueError):
         cohort.ensemble_roc_auc(coh, zoo.Selector.ones(3))
     assert cohort.ensemble_roc_auc(coh, zoo.Selector.ones(2)) == 0.5   # all tied
+
+
+def test_one_shot_hb_sweep_auc_matches_oracle_and_cohort_path(c4):
+    """The one-shot C-ABI entry `hb_sweep_auc` (32-bit selector masks) gives the same AUCs as the
+    persistent-cohort path and the CPU oracle, bit for bit."""
+    z10, coh = c4
+    masks = np.arange(1, 1024, 7, dtype=np.uint32)
+    got = metrics.sweep_auc(coh.labels, coh.scores, masks)
+    assert np.array_equal(got, oauc.sweep(coh.labels, coh.scores, masks.astype(np.int64)))
+    assert np.array_equal(got, composer.sweep_aucs(coh)[masks - 1])
+
+
+def test_n16_sweep_and_selection_match_reference_bit_exact():
+    """c4 at n = 16: all 65 535 candidates' AUCs equal the reference's exhaustive_search
+    (tests/golden/sweep_n16.npz, N = 20 000) bit for bit, and so does the selected ensemble with
+    the reference's latency values."""
+    z16 = zoo.generate_zoo(1, [8, 16, 32, 64], [2, 4, 8, 16], seed=3)
+    coh = cohort.synthesize_cohort(z16, 10000, 10000, 0.5, 0)
+    gold = np.load(os.path.join(G, "sweep_n16.npz"))
+    aucs = composer.sweep_aucs(coh)
+    assert aucs.shape == (65535,)
+    bad = np.flatnonzero(aucs != gold["auc"])
+    assert bad.size == 0, (bad[:10], aucs[bad[:3]], gold["auc"][bad[:3]])
+    lat = gold["latency"]
+    res = composer.exhaustive_search(z16, coh, lambda b: float(lat[b.as_int() - 1]), budget_s=0.2)
+    assert res.best.as_int() == int(gold["best"][0])
+    assert res.best_objective == float(gold["best_objective"][0])

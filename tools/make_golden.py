@@ -21,6 +21,9 @@ Fixtures:
                     latency and the selected ensemble                 (composer.py:597-638)
   sweep_ties.npz    exhaustive_search AUCs on a tie-heavy cohort (n=8)
   latency.json      service_time / measure_capacity / LatencyProfiler (latency.py:145-333)
+  curves.npz        build_arrival_curve on profiling traces of 16..8192 beds: the exact
+                    branch and the binned branch above 8000 events (latency.py:198-239)
+  sweep_n16.npz     exhaustive_search at n = 16 (65 535 candidates, N = 20 000)
 """
 from __future__ import annotations
 
@@ -243,8 +246,41 @@ def gen_latency():
     dump("latency.json", out)
 
 
+def gen_curves():
+    """The reference's build_arrival_curve on profiling traces of growing bed counts: exact branch
+    (<= 8000 events) and the binned branch (latency.py:223-239) at 4100 and 8192 beds."""
+    out = {}
+    for beds in (16, 64, 1024, 4000, 4100, 8192):
+        sysc = rl.SystemConfig(patients=beds)
+        ts = rl.profiling_trace(sysc, seed=7)
+        a = rl.build_arrival_curve(ts)
+        out[f"b{beds}_dts"] = np.asarray(a.dts)
+        out[f"b{beds}_counts"] = np.asarray(a.counts)
+        out[f"b{beds}_meta"] = np.array([a.n_events, a.span_s])
+    np.savez_compressed(os.path.join(OUT, "curves.npz"), **out)
+
+
+def gen_sweep_n16():
+    """exhaustive_search at n = 16 (65 535 candidates) over the c4-sized cohort (N = 20 000)."""
+    zoo16 = rz.generate_zoo(1, [8, 16, 32, 64], [2, 4, 8, 16], seed=3)
+    c = rc.synthesize_cohort(zoo16, 10000, 10000, correlation=0.5, seed=0)
+    sysc = rl.SystemConfig()
+    lp = rl.LatencyProfiler(zoo16, rl.ExecutorModel(), sysc)
+    res = rcomp.exhaustive_search(zoo16, c, lp, budget_s=sysc.budget_s, sys=sysc)
+    np.savez_compressed(os.path.join(OUT, "sweep_n16.npz"),
+                        auc=np.array([r.accuracy for r in res.profiled]),
+                        latency=np.array([r.latency_s for r in res.profiled]),
+                        best=np.array([sum(b << k for k, b in enumerate(res.best.bits))]),
+                        best_objective=np.array([res.best_objective]), best_accuracy=np.array([res.best_accuracy]),
+                        scores_sha=np.array([sha(c.scores)]))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1:          # regenerate only the named fixtures, e.g. `make_golden.py curves sweep_n16`
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        return
     gen_seeds()
     gen_zoos()
     gen_windows()
@@ -253,6 +289,8 @@ def main():
     gen_cohort()
     gen_latency()
     gen_sweeps()
+    gen_curves()
+    gen_sweep_n16()
     with open(os.path.join(OUT, "VERSIONS.json"), "w") as fh:
         import sklearn
         json.dump({"numpy": np.__version__, "sklearn": sklearn.__version__, "python": sys.version.split()[0],
