@@ -180,14 +180,39 @@ def _bits(cohort: Cohort, b: Selector) -> np.ndarray:
     return np.array(b.bits, dtype=np.uint8)
 
 
+MAX_DEVICE_COLUMNS = 256   # the K6 kernel's column list (csrc/sweep.cu kMaxCols)
+
+
+def _device_and_bits(cohort: Cohort, b: Selector, device: int):
+    """The device cohort and selector bits to score b with.  Cohorts wider than the kernel's column
+    list (the reference accepts any width) are scored on a device sub-cohort of just the selected
+    columns, in column order (so the fp64 mean sums in the same order), cached per column set."""
+    bits = _bits(cohort, b)
+    if cohort.n_models <= MAX_DEVICE_COLUMNS:
+        return cohort.device(device), bits
+    cols = tuple(int(i) for i in np.flatnonzero(bits))
+    if len(cols) > MAX_DEVICE_COLUMNS:
+        raise ValueError(f"an ensemble of {len(cols)} members exceeds the device sweep's "
+                         f"{MAX_DEVICE_COLUMNS} columns")
+    cache = cohort._dev.setdefault(("wide", device), {})
+    dev = cache.get(cols)
+    if dev is None:
+        if len(cache) >= 16:
+            cache.pop(next(iter(cache))).close()
+        dev = cache[cols] = DeviceCohort(np.ascontiguousarray(cohort.scores[:, cols]), cohort.labels, device)
+    return dev, np.ones(len(cols), np.uint8)
+
+
 def ensemble_scores(cohort: Cohort, b: Selector, device: int = 0) -> np.ndarray:
     """Per-sample mean of the selected members' scores (device, column order fp64)."""
-    return cohort.device(device).ensemble(_bits(cohort, b))[0]
+    dev, bits = _device_and_bits(cohort, b, device)
+    return dev.ensemble(bits)[0]
 
 
 def ensemble_roc_auc(cohort: Cohort, b: Selector, device: int = 0) -> float:
     """ROC-AUC of the ensemble mean: the accuracy profiler's value (device)."""
-    return float(cohort.device(device).auc_bits(_bits(cohort, b)[None, :])[0])
+    dev, bits = _device_and_bits(cohort, b, device)
+    return float(dev.auc_bits(bits[None, :])[0])
 
 
 def accuracy_profile(cohort: Cohort, b: Selector, device: int = 0) -> AccuracyReport:
@@ -238,3 +263,12 @@ def record_cohort(zoo: ModelZoo, windows: np.ndarray, labels, *, selector: Selec
             k = min(P, N - r0)
             out[r0:r0 + k] = res.member_logits[:k]
     return Cohort(labels=np.asarray(labels, np.int8), scores=out, seed=seed)
+
+
+def save_cohort_csv(cohort: Cohort, path) -> None:
+    """label,score_0..score_{n-1} rows, repr() floats (cohort.py:118-124)."""
+    import csv
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh)
+        w.writerow(["label"] + [f"score_{j}" for j in range(cohort.n_models)])
+        w.writerows([int(lab)] + [repr(float(v)) for v in row] for lab, row in zip(cohort.labels, cohort.scores))

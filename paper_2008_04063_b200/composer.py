@@ -125,11 +125,20 @@ class SearchResult:
             json.dump(self.to_json_dict(), fh, indent=2, sort_keys=True)
             fh.write("\n")
 
+    def save_trajectory_csv(self, path) -> None:
+        """iter,best_acc,best_lat,best_obj rows with repr() floats (composer.py:138-143)."""
+        rows = ["iter,best_acc,best_lat,best_obj"]
+        rows += [f"{p.iteration},{p.best_accuracy!r},{p.best_latency_s!r},{p.best_objective!r}"
+                 for p in self.trajectory]
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("\n".join(rows) + "\n")
+
 
 def constraint_penalty(x: float, mode: str = HARD, weight: float = 1.0) -> float:
-    """Penalty of constraint slack x: -inf below zero (hard) or weight * x (soft)."""
+    """Penalty of constraint slack x: -inf below zero (hard) or weight * x (soft).  The hard test is
+    `x < 0` as in the reference (composer.py:146-152): a NaN slack (inf budget - inf latency) is 0."""
     if mode == HARD:
-        return 0.0 if x >= 0 else -math.inf
+        return -math.inf if x < 0 else 0.0
     if mode == SOFT:
         return weight * x
     raise ValueError(f"unknown constraint mode {mode!r}")

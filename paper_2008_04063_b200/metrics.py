@@ -91,6 +91,23 @@ def f1_accuracy(labels, scores, threshold: float = 0.5) -> tuple[float, float]:
     return ((2 * tp / denom) if denom else 0.0), float(np.mean(pred == actual))
 
 
+def r2(predicted, actual) -> float:
+    """Coefficient of determination 1 - SS_res / SS_tot (metrics.py:114-127): 1-D, equal length,
+    >= 2 samples; constant actuals raise UndefinedMetricError."""
+    pr = np.asarray(predicted, dtype=np.float64)
+    ac = np.asarray(actual, dtype=np.float64)
+    if pr.ndim != 1 or pr.shape != ac.shape:
+        raise ValueError("predicted and actual must be 1-D and the same length")
+    if ac.size < 2:
+        raise ValueError("need at least two samples")
+    centred = ac - ac.mean()
+    ss_tot = float(np.sum(centred * centred))
+    if ss_tot == 0.0:
+        raise UndefinedMetricError("r2 undefined for constant actuals")
+    resid = ac - pr
+    return 1.0 - float(np.sum(resid * resid)) / ss_tot
+
+
 def sweep_auc(labels, score_matrix, selectors, device: int = 0) -> np.ndarray:
     """AUC of the ensemble mean of every selector, one shot through the C-ABI's `hb_sweep_auc`
     (the batched accuracy pass of `exhaustive_search`, composer.py:614-619): `selectors` are

@@ -22,9 +22,10 @@ that tick.  With `hop < window` the engine scores a sliding window every hop.
 from __future__ import annotations
 
 import heapq
+import json
 import math
 from collections import deque
-from dataclasses import dataclass
+from dataclasses import asdict, dataclass
 
 import numpy as np
 
@@ -341,3 +342,51 @@ def e2e_percentiles(traces: list) -> dict:
 
 def queueing_delays(traces: list) -> list:
     return [t.t_dequeue - t.t_enqueue for t in traces]
+
+
+def save_traces_jsonl(traces: list, path) -> None:
+    """One JSON object per trace, keys sorted (runtime.py:259-264)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(json.dumps(asdict(t), sort_keys=True) + "\n" for t in traces)
+
+
+@dataclass(frozen=True)
+class TimelinePoint:
+    t_s: float
+    latency_s: float
+    kind: str    # "aggregation" or "inference"
+
+
+def batch_comparison(zoo: ModelZoo, b: Selector, executor: ExecutorModel, patients: int, rates: dict,
+                     window_s: float, batch_period_s: float, duration_s: float, seed: int = 0,
+                     agg_overhead_s: float = DEFAULT_AGG_OVERHEAD_S) -> tuple[list, list]:
+    """Online per-window serving vs deferred batch processing (runtime.py:273-311), host only.
+
+    Both timelines come from the parity-mode DES of the same seeded windows: online = one
+    inference point per query (done - enqueue at its enqueue time); batch = at every period
+    boundary the queries enqueued in that period drained back to back through the slots;
+    plus one aggregation-only point per simulated second on both."""
+    if batch_period_s < window_s:
+        raise ConfigurationError("batch_period_s must be >= window_s")
+    traces = run_simulation(zoo, b, executor, patients, rates, window_s, duration_s, seed=seed,
+                            agg_overhead_s=agg_overhead_s)
+    s_q = service_time(b, zoo, executor)
+    online = [TimelinePoint(t.t_enqueue, t.t_done - t.t_enqueue, "inference") for t in traces]
+    batch = []
+    for m in range(1, int(math.floor(duration_s / batch_period_s + 1e-9)) + 1):
+        hi = m * batch_period_s
+        n = sum(1 for t in traces if hi - batch_period_s < t.t_enqueue - agg_overhead_s <= hi)
+        if n:
+            batch.append(TimelinePoint(hi, agg_overhead_s + math.ceil(n / executor.n_slots) * s_q, "inference"))
+    for sec in range(int(duration_s)):
+        online.append(TimelinePoint(float(sec), agg_overhead_s, "aggregation"))
+        batch.append(TimelinePoint(float(sec), agg_overhead_s, "aggregation"))
+    key = lambda pt: (pt.t_s, pt.kind)  # noqa: E731
+    return sorted(online, key=key), sorted(batch, key=key)
+
+
+def save_timeline_csv(points: list, path) -> None:
+    """t_s,latency_s,kind rows with repr() floats (runtime.py:314-318)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("t_s,latency_s,kind\n")
+        fh.writelines(f"{p.t_s!r},{p.latency_s!r},{p.kind}\n" for p in points)

@@ -144,3 +144,27 @@ def test_n16_sweep_and_selection_match_reference_bit_exact():
     res = composer.exhaustive_search(z16, coh, lambda b: float(lat[b.as_int() - 1]), budget_s=0.2)
     assert res.best.as_int() == int(gold["best"][0])
     assert res.best_objective == float(gold["best_objective"][0])
+
+
+def test_trajectory_csv_of_a_device_search_matches_reference_bytes(tmp_path):
+    import json
+    g = json.load(open(os.path.join(G, "helpers.json")))
+    z10 = zoo.generate_zoo(1, [8, 16, 32, 64, 128], [2, 4], seed=3)
+    c10 = cohort.synthesize_cohort(z10, 300, 300, 0.5, 0)
+    res = composer.exhaustive_search(z10, c10, lambda s: 0.01 * sum(s.bits), budget_s=0.05)
+    res.save_trajectory_csv(tmp_path / "t.csv")
+    assert (tmp_path / "t.csv").read_text(encoding="utf-8") == g["trajectory_csv"]
+
+
+def test_cohorts_wider_than_the_kernel_column_list():
+    """The reference accepts any cohort width; a 300-column cohort is scored on device sub-cohorts
+    of the selected columns, bit-exact against the oracle."""
+    rng = np.random.default_rng(3)
+    lab = (rng.random(3000) < 0.45).astype(np.int8)
+    sc = rng.standard_normal((3000, 300)) + 0.3 * lab[:, None]
+    coh = cohort.Cohort(labels=lab, scores=sc, seed=0)
+    for cols in ([0], [5, 299], list(range(0, 300, 7)), [17, 18, 19, 250]):
+        b = zoo.Selector.from_indices(300, cols)
+        v = int(sum(1 << c for c in cols))
+        assert cohort.ensemble_roc_auc(coh, b) == oauc.sweep(lab, sc, [v])[0]
+        assert np.array_equal(cohort.ensemble_scores(coh, b), oauc.ensemble_mean(sc, cols))

@@ -24,6 +24,8 @@ Fixtures:
   curves.npz        build_arrival_curve on profiling traces of 16..8192 beds: the exact
                     branch and the binned branch above 8000 events (latency.py:198-239)
   sweep_n16.npz     exhaustive_search at n = 16 (65 535 candidates, N = 20 000)
+  helpers.json      save_traces_jsonl, batch_comparison + save_timeline_csv, save_cohort_csv,
+                    SearchResult.save_trajectory_csv, curves_to_csv, r2, constraint_penalty(nan)
 """
 from __future__ import annotations
 
@@ -275,6 +277,42 @@ def gen_sweep_n16():
                         scores_sha=np.array([sha(c.scores)]))
 
 
+def gen_helpers():
+    """The reference's host-side I/O helpers and small metrics, as file contents / values: traces
+    JSONL, batch_comparison timelines CSV, cohort CSV, trajectory CSV, curves CSV, r2, and the hard
+    constraint penalty on a NaN slack."""
+    import tempfile
+    out = {}
+    zoo = rz.generate_zoo(3, [8, 16, 32, 64, 128], [2, 4, 8, 16], seed=1)
+    b = rz.Selector.from_indices(60, [10, 13, 30, 50])
+    rates = {"ECG-I": 250.0, "ECG-II": 250.0, "ECG-III": 250.0}
+    ex = rl.ExecutorModel(n_slots=2)
+    with tempfile.TemporaryDirectory() as d:
+        def text(fn, *a):
+            path = os.path.join(d, "f")
+            fn(*a, path)
+            return open(path, encoding="utf-8").read()
+        tr = rr.run_simulation(zoo, b, ex, 3, rates, 30.0, 90.0, seed=4)
+        out["traces_jsonl"] = text(rr.save_traces_jsonl, tr)
+        on, ba = rr.batch_comparison(zoo, b, ex, 5, rates, 30.0, 120.0, 600.0, seed=2)
+        out["timeline_online_csv"] = text(rr.save_timeline_csv, on)
+        out["timeline_batch_csv"] = text(rr.save_timeline_csv, ba)
+        c = rc.synthesize_cohort(rz.generate_zoo(1, [8, 16], [2], seed=3), 6, 5, correlation=0.5, seed=1)
+        out["cohort_csv"] = text(rc.save_cohort_csv, c)
+        zoo10 = rz.generate_zoo(1, [8, 16, 32, 64, 128], [2, 4], seed=3)
+        c10 = rc.synthesize_cohort(zoo10, 300, 300, correlation=0.5, seed=0)
+        res = rcomp.exhaustive_search(zoo10, c10, lambda s: 0.01 * sum(s.bits), budget_s=0.05)
+        out["trajectory_csv"] = text(lambda p: res.save_trajectory_csv(p))
+        ts = rl.profiling_trace(rl.SystemConfig(patients=16), seed=3)
+        out["curves_csv"] = text(rl.curves_to_csv, rl.build_arrival_curve(ts),
+                                 rl.ServiceCurve(rate_qps=5.0, latency_offset_s=0.01))
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal(50)
+    out["r2"] = [rm.r2(a + 0.1 * rng.standard_normal(50), a), rm.r2(a[::-1].copy(), a)]
+    out["penalty_nan_slack"] = rcomp.constraint_penalty(float("nan"))
+    dump("helpers.json", out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1:          # regenerate only the named fixtures, e.g. `make_golden.py curves sweep_n16`
@@ -291,6 +329,7 @@ def main():
     gen_sweeps()
     gen_curves()
     gen_sweep_n16()
+    gen_helpers()
     with open(os.path.join(OUT, "VERSIONS.json"), "w") as fh:
         import sklearn
         json.dump({"numpy": np.__version__, "sklearn": sklearn.__version__, "python": sys.version.split()[0],
