@@ -80,5 +80,7 @@ def test_gpus2_relaunches_under_torchrun_and_refuses_without_devices():
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
                        capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
     assert p.returncode != 0
-    # both ranks of the relaunch saw WORLD_SIZE=2 and refused on the device count, not the world size
-    assert p.stderr.count("refusing to run: --gpus 2 but only 0 CUDA device(s) are visible") == 2, p.stderr[-2000:]
+    # the relaunched ranks saw WORLD_SIZE=2 and refused on the device count, not the world size
+    # (torchrun tears the group down after the first failing rank, so one or both report)
+    assert p.stderr.count("refusing to run: --gpus 2 but only 0 CUDA device(s) are visible") >= 1, p.stderr[-2000:]
+    assert "WORLD_SIZE=1" not in p.stderr and "--nproc-per-node" not in p.stderr
