@@ -117,6 +117,35 @@ def test_c3_full_zoo_100_beds_sampled():
     _run(Selector.ones(60), 100, 250, 1, 2, [0, 33, 50, 71, 99], xn_check=True)
 
 
+@pytest.mark.parametrize("hop", [249, 251, 7500])
+def test_window_alignment_and_warmup(hop):
+    """The vectorised window kernel reads 16-B aligned float4s and shifts by the window start's
+    misalignment (start mod 4, uniform per tick).  An odd hop walks the start through all four
+    residues; ticks from an EMPTY ring put the window start before the stream's first sample
+    (zeros, `oracle.windows.sliding_window`).  Raw samples bit-exact, fp16 z-norm within 1 ulp,
+    and the tick's scores against the oracle at the last tick."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, [10])
+    P, ticks = 3, 5 if hop < W else 2
+    streams = synth.ecg_block(21, P, 3, 0, ticks * hop)
+    residues = set()
+    with EnsembleEngine(zoo, sel, P, hop=hop, keep_windows=True) as eng:
+        for k in range(ticks):
+            end = (k + 1) * hop
+            res = eng.tick(streams[:, :, end - hop:end])
+            residues.add((end - W) % 4)
+            raw, _ = eng.last_windows()
+            for p in range(P):
+                for lead in range(3):
+                    assert np.array_equal(raw[p, lead], windows.sliding_window(streams[p, lead], end, W)), (k, p)
+            _check_xn(eng.last_normalized(), streams, end, list(range(P)))
+    ml, prob, mlog = cpu_path.cpu_tick(zoo, sel, streams, end, beds=list(range(P)))
+    _compare(res.member_logits, res.ens_prob, res.ens_mean_logit, ml, prob, mlog)
+    if hop < W:
+        assert residues == {0, 1, 2, 3}
+
+
 @pytest.mark.parametrize("lane_sms", ["3", "4", "6", "9"])
 def test_k4b_multi_tile_paths_forced(monkeypatch, lane_sms):
     """Cap every conv grid at a few CTAs (HB_LANE_SMS) so that at 5 beds each persistent CTA
@@ -142,6 +171,9 @@ STATIC_KNOBS = [
     {"HB_PP_STAGES": "2"},                    # shallowest B pipeline
     {"HB_PP_RES_EPI": "1"},                   # identity shortcut in the epilogue instead of MMAs
     {"HB_WIN": "1"},                          # shared-memory window kernel
+    {"HB_WIN": "2"},                          # scalar register window kernel (pre-vectorisation)
+    {"HB_WIN_NB": "3"},                       # TMA window kernel, 3 buffers (two streams of look-ahead)
+    {"HB_WIN_NB": "1"},                       # TMA window kernel, 1 buffer (no look-ahead, 6 CTAs/SM)
 ]
 
 
