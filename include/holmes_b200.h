@@ -126,6 +126,12 @@ int hb_last_tick_ms(hb_ctx* ctx, float* ms);
 /* Median device milliseconds of `reps` tick-graph launches on the context's
  * stream (after one warm-up launch).  Measures; the stream cursor advances. */
 int hb_time_tick(hb_ctx* ctx, int reps, float* median_ms);
+/* Build the current selection's tick graphs (if the selection or a member
+ * changed) and upload them to the device, without running a tick: a serving
+ * loop calls it before its clock starts so the first tick is not charged the
+ * one-off plan/capture/instantiate cost (replaces nothing in the reference,
+ * whose scorer has no setup, runtime.py:121-129). */
+int hb_prepare(hb_ctx* ctx);
 
 /* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
  * (mean, std) [P][n_leads][2] of the most recent tick. */

@@ -922,6 +922,19 @@ int hb_time_tick(hb_ctx* c, int reps, float* median_ms) {
   return HB_OK;
 }
 
+int hb_prepare(hb_ctx* c) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  cudaSetDevice(c->device);
+  if (c->dirty && (c->io_busy[0] || c->io_busy[1]))
+    return fail(c, HB_E_STATE, "the selection changed while a submitted tick is uncollected; collect it first");
+  const int rc = build_selection(c);
+  if (rc) return rc;
+  CK(c, cudaGraphUpload(c->graph, c->own));
+  for (int k = 0; k < 2; ++k) CK(c, cudaGraphUpload(c->graph_io[k], c->own));
+  CK(c, cudaStreamSynchronize(c->own));
+  return HB_OK;
+}
+
 int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {
   if (!c || !c->member_logits) return HB_E_STATE;
   if (ml) *ml = c->member_logits;

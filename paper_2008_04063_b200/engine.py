@@ -120,6 +120,12 @@ class EnsembleEngine:
             raise ValueError(f"expected samples of shape {(self.patients, self.leads, n)}, got {a.shape}")
         return a
 
+    def prepare(self) -> None:
+        """Plan, capture and upload the tick graphs of the current selection now
+        (`hb_prepare`), so the next tick is not charged the one-off setup."""
+        with self._lock:
+            _lib.check(_lib.lib().hb_prepare(self._h), self._h)
+
     def ingest(self, samples) -> None:
         """Append [P, leads, n] samples to every stream without scoring (warm-up / catch-up)."""
         a = np.ascontiguousarray(samples, dtype=np.float32)

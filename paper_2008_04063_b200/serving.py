@@ -45,6 +45,7 @@ class ServingLoop:
         if prefill and eng.window > eng.hop:
             eng.ingest(self.source(0, eng.window - eng.hop))
             pos = eng.window - eng.hop
+        eng.prepare()  # graphs built and uploaded before the clock starts
         traces: list = []
         t0 = time.monotonic()
         frames = [self.source(pos + k * eng.hop, eng.hop) for k in range(n_ticks)]  # the sensors' future data
