@@ -132,6 +132,13 @@ int hb_time_tick(hb_ctx* ctx, int reps, float* median_ms);
  * one-off plan/capture/instantiate cost (replaces nothing in the reference,
  * whose scorer has no setup, runtime.py:121-129). */
 int hb_prepare(hb_ctx* ctx);
+/* Diagnostics of the chain launch (K4c, HB_CHAIN=1 with HB_CHAIN_PROF=1 set
+ * before the selection is built): per CTA 16 counters of the last tick
+ * (producer dependency-wait / weight-wait / stage-wait / total cycles, items,
+ * MMA weight-wait / accumulator-wait / stage-wait / total, epilogue
+ * accumulator-wait / total).  Returns the grid size (0 = no chain or no
+ * profiling), copies min(grid, cap) rows. */
+int hb_chain_profile(hb_ctx* ctx, unsigned long long* out, int cap);
 
 /* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
  * (mean, std) [P][n_leads][2] of the most recent tick. */

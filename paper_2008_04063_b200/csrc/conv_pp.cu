@@ -51,6 +51,7 @@
 // mean-pool . FC into one partial per (tile, column half, warp).
 #include <algorithm>
 #include <functional>
+#include <vector>
 
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
@@ -101,6 +102,210 @@ __device__ __forceinline__ CtaRange cta_range(const PPArgs& a) {
     r.end = (g + 1) * per_g;
   }
   return r;
+}
+
+// MMAs of one staged 16-channel pair (or one shortcut pair), issued by the
+// calling (elected) lane, then one commit to the stage's empty barrier.
+// Descriptors advance on their low words only (the 14-bit start-address
+// field; shared addresses never carry out of it): A by one tap-array entry per
+// shift (stride 2: alternating parity arrays, w_par16 apart), B by one phase
+// plane per shift and by one row, back to phase 0, when the phase wraps.  The
+// issue loop is on the MMA's critical path (measured: one extra uniform
+// instruction per MMA cost 6 % of the c2 tick), hence no per-MMA election,
+// division or modulo.
+__device__ __forceinline__ void pp_issue_pair(const PPArgs& a, uint32_t d_tmem, uint64_t a0, uint64_t b0,
+                                              uint32_t idesc, bool first, uint64_t* empty_bar) {
+  const uint64_t a_hi = a0 & 0xFFFFFFFF00000000ull, b_hi = b0 & 0xFFFFFFFF00000000ull;
+  const int Q = a.Q, R = a.R, pad = a.pad;
+  int q = (-pad) & (Q - 1);
+  uint32_t b_lo = static_cast<uint32_t>(b0) + static_cast<uint32_t>(q * R + 8 + ((-pad) >> a.qs));
+  const uint32_t b_wrap = static_cast<uint32_t>(1 - (Q - 1) * R), b_step = static_cast<uint32_t>(R);
+  uint32_t a_lo = static_cast<uint32_t>(a0);
+  const uint32_t a_step = static_cast<uint32_t>(a.cout);
+  uint32_t acc = first ? 0u : 1u;
+  auto adv_b = [&]() {
+    if (q == Q - 1) {
+      q = 0;
+      b_lo += b_wrap;
+    } else {
+      ++q;
+      b_lo += b_step;
+    }
+  };
+  if (a.stride == 1) {
+    for (int u = 0; u < a.U; ++u) {
+      mma_f16_ss(d_tmem, a_hi | a_lo, b_hi | b_lo, idesc, acc);
+      acc = 1u;
+      a_lo += a_step;
+      adv_b();
+    }
+  } else {  // U even: shift u uses parity u & 1, entry u >> 1
+    const uint32_t par = a.w_par16;
+    for (int u = 0; u < a.U; u += 2) {
+      mma_f16_ss(d_tmem, a_hi | a_lo, b_hi | b_lo, idesc, acc);
+      acc = 1u;
+      adv_b();
+      mma_f16_ss(d_tmem, a_hi | (a_lo + par), b_hi | b_lo, idesc, 1u);
+      adv_b();
+      a_lo += a_step;
+    }
+  }
+  mma_commit(empty_bar);
+}
+
+// One tile's epilogue for the calling warpgroup (one half of the tile's
+// columns): TMEM -> + bias -> fp16 -> 8x8 register transpose -> + shortcut,
+// ReLU -> 16-B row stores, or (a member's last conv) the fused mean-pool . FC
+// partial.  After the transpose, lane (M row (p', c), column octet r8) covers
+// positions l = l0 + h * step, h = 2 * chunk + b, step = 8 * ph; every Q-phase
+// layout involved has Q | step (Q <= 32, checked by the planner), so each load
+// and store address is a per-tile base + h * a constant and the bounds checks
+// are h < h_valid (l < lout) / h < h_rows (l < out_rows).  The per-chunk work
+// is then the TMEM load, bias, conversion, transpose and shortcut math only --
+// the 64-bit Q-phase address arithmetic per access made the epilogue
+// instruction-issue bound (~275 SASS per chunk, as many issue cycles as the
+// MMAs of the tile at 32 channels).
+// kLateRes: read the shortcut only after the accumulator wait (K4c: the rows
+// are written inside the same launch); otherwise the first two chunks' rows
+// are requested before it.  Returns after arriving on acc_empty.
+template <bool kLateRes>
+__device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, int ew, int wq, int lane,
+                                            uint32_t taddr, uint64_t* acc_full, uint32_t accph,
+                                            uint64_t* acc_empty, float bias, bool cg, bool skip_math) {
+  const int cout = a.cout, ph = a.ph;
+  const int row = wq * 32 + lane;  // M row = (p', c)
+  const int lc = __ffs(cout) - 1;
+  const int c = row & (cout - 1);
+  const int phase = ph - 1 - (row >> lc);
+  const int g8 = c >> 3;
+  const int r8 = lane & 7;
+  const int nch = a.nb >> 4;  // 16-column chunks; this warpgroup takes half (the first the larger)
+  const int c_lo = (ew >> 1) ? (nch + 1) >> 1 : 0, c_hi = (ew >> 1) ? nch : (nch + 1) >> 1;
+  const int step = 8 * ph;
+  const int l0 = ph * (t.nt * a.nb + r8) + phase;
+  const int h_valid = l0 < a.lout ? (a.lout - l0 + step - 1) / step : 0;
+  const int h_rows = l0 < a.out_rows ? (a.out_rows - l0 + step - 1) / step : 0;
+  const int res_mode = a.res_mode;
+  const bool has_res = res_mode != 0 && g8 * 8 < a.res_c;
+  const __half* r0p = a.res;
+  const __half* r1p = a.res;
+  int r_inc = 0;
+  if (has_res) {
+    const size_t res_plane = static_cast<size_t>(t.p) * (a.res_c >> 3) + g8;
+    if (res_mode == 2) {
+      r0p = a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l0);
+      r1p = a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l0 + 1);
+      r_inc = ((2 * step) >> a.res_qs) * 8;
+    } else {
+      r0p = a.res + q_off(res_plane, a.res_qs, a.res_lq, l0);
+      r_inc = (step >> a.res_qs) * 8;
+    }
+  }
+  const float* fcw = a.fc_w;
+  __half* outp = fcw ? nullptr : a.out + q_off(static_cast<size_t>(t.p) * (cout >> 3) + g8, a.out_qs, a.out_lq, l0);
+  const int o_inc = (step >> a.out_qs) * 8;
+  float head = 0.f;
+  float fc8[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) fc8[q] = fcw ? __ldg(fcw + static_cast<size_t>(t.g) * cout + g8 * 8 + q) : 0.f;
+  // Shortcut rows (2 positions per lane and chunk; maxpool reads 2 rows each)
+  // are loaded two chunks ahead through two register sets (the chunk loop is
+  // unrolled by two so both stay in registers).
+  uint4 rawA[4], rawB[4];
+  auto ld = [&](const __half* p) {
+    return cg ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
+  };
+  auto load_res = [&](int ch, uint4 (&raw)[4]) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int h = 2 * ch + b;
+      const bool ok = has_res && h < h_valid;
+      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      raw[2 * b] = ok ? ld(r0p + h * r_inc) : z;
+      if (res_mode == 2) raw[2 * b + 1] = ok ? ld(r1p + h * r_inc) : z;
+    }
+  };
+  if (!kLateRes && res_mode) {
+    load_res(c_lo, rawA);
+    if (c_lo + 1 < c_hi) load_res(c_lo + 1, rawB);
+  }
+  mbar_wait(acc_full, accph, 120);
+  tc_fence_after();
+  if (kLateRes && res_mode) {
+    load_res(c_lo, rawA);
+    if (c_lo + 1 < c_hi) load_res(c_lo + 1, rawB);
+  }
+  auto chunk = [&](int ch, uint4 (&raw)[4]) {
+    uint32_t r[16];
+    tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 16), r);
+    uint4 rv[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (res_mode == 2) {
+        const __half2* h0 = reinterpret_cast<const __half2*>(&raw[2 * b]);
+        const __half2* h1 = reinterpret_cast<const __half2*>(&raw[2 * b + 1]);
+        __half2* o2 = reinterpret_cast<__half2*>(&rv[b]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o2[q] = __hmax2(h0[q], h1[q]);
+      } else {
+        rv[b] = res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    if (res_mode && ch + 2 < c_hi) load_res(ch + 2, raw);
+    tmem_wait_ld();
+    if (ch == c_hi - 1) {  // this warpgroup's columns drained
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+    if (skip_math) return;
+    // (acc + bias) is rounded to fp16 before the transpose; the shortcut add
+    // and ReLU run on half2 (two roundings instead of one: within one fp16 ulp
+    // of the fp32 reference, tests/test_conv_pp_gpu.py).
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int h = 2 * ch + b;
+      uint32_t hv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __half2 v2 = __floats2half2_rn(__uint_as_float(r[8 * b + 2 * q]) + bias,
+                                             __uint_as_float(r[8 * b + 2 * q + 1]) + bias);
+        hv[q] = *reinterpret_cast<const uint32_t*>(&v2);
+      }
+      transpose8_h2(hv, r8);
+      if (h < h_rows) {
+        const __half2* rr = reinterpret_cast<const __half2*>(&rv[b]);
+        const __half2 zero = __float2half2_rn(0.f);
+        const bool valid = h < h_valid;
+        uint4 pk;
+        __half2* o2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __half2 y = __hmax2(__hadd2(*reinterpret_cast<const __half2*>(&hv[q]), rr[q]), zero);
+          o2[q] = valid ? y : zero;
+        }
+        if (outp != nullptr) {
+          *reinterpret_cast<uint4*>(outp + h * o_inc) = pk;
+        } else if (valid) {  // fused head: this position's 8 channels . fc
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __half22float2(o2[q]);
+            head = fmaf(f.x, fc8[2 * q], fmaf(f.y, fc8[2 * q + 1], head));
+          }
+        }
+      }
+    }
+  };
+  for (int ch = c_lo; ch < c_hi; ch += 2) {
+    chunk(ch, rawA);
+    if (ch + 1 < c_hi) chunk(ch + 1, rawB);
+  }
+  if (fcw != nullptr) {  // one partial per (tile, epilogue warp), summed in fixed order by K5
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) head += __shfl_xor_sync(0xffffffffu, head, off);
+    if (lane == 0)
+      a.head_out[static_cast<size_t>(t.g) * a.head_g_stride + static_cast<size_t>(t.p - t.g * a.Pm) * a.head_mt +
+                 static_cast<size_t>(t.nt) * 8 + (ew >> 1) * 4 + wq] = head;  // (column half, warp)
+  }
 }
 
 __global__ void __launch_bounds__(kPPThreads, 1)
@@ -233,29 +438,23 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         }
         tc_fence_after();
         const uint64_t b0 = make_desc(smem_u32(sB + static_cast<size_t>(st) * a.stage_bytes), b_lbo, 128);
-        if (j >= a.n_pairs) {
-          // identity shortcut on the tensor core: D[(p', c), n] += x[c, ph*n + p] as one K=16 MMA per
-          // phase p, A = the phase-p window of the selection array Z (ones at (p', c) -> channel c)
-          const uint64_t z0 = make_desc(smem_u32(sW) + a.z_off + static_cast<uint32_t>(j - a.n_pairs) * a.z_pair_bytes,
-                                        a.z_half_bytes, 128);
-          for (int ps = 0; ps < a.ph; ++ps) {
-            if (!(a.dbg & 2) && elect_one())
+        if (elect_one()) {
+          if (a.dbg & 2) {
+            mma_commit(&st_empty[st]);
+          } else if (j >= a.n_pairs) {
+            // identity shortcut on the tensor core: D[(p', c), n] += x[c, ph*n + p] as one K=16 MMA per
+            // phase p, A = the phase-p window of the selection array Z (ones at (p', c) -> channel c)
+            const uint64_t z0 = make_desc(smem_u32(sW) + a.z_off + static_cast<uint32_t>(j - a.n_pairs) * a.z_pair_bytes,
+                                          a.z_half_bytes, 128);
+            for (int ps = 0; ps < a.ph; ++ps)
               mma_f16_ss(d_tmem, z0 + static_cast<uint32_t>(ps * a.cout), b0 + static_cast<uint32_t>(ps * a.R + 8),
                          idesc, 1u);
+            mma_commit(&st_empty[st]);
+          } else {
+            const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
+            pp_issue_pair(a, d_tmem, a0, b0, idesc, j == 0, &st_empty[st]);
           }
-        } else {
-        const uint64_t a0 = make_desc(smem_u32(sW) + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
-        for (int u = 0; u < a.U; ++u) {
-          const int pi = (a.stride == 2) ? (u & 1) : 0;
-          const uint32_t aoff = static_cast<uint32_t>(pi) * a.w_par16 +
-                                static_cast<uint32_t>((u - pi) >> (a.stride - 1)) * static_cast<uint32_t>(a.cout);
-          const int v = u - a.pad;
-          const uint32_t boff = static_cast<uint32_t>((v & (a.Q - 1)) * a.R + 8 + (v >> a.qs));
-          if (!(a.dbg & 2) && elect_one()) mma_f16_ss(d_tmem, a0 + aoff, b0 + boff, idesc, (j | u) ? 1u : 0u);
         }
-        }
-        __syncwarp();
-        if (elect_one()) mma_commit(&st_empty[st]);
         __syncwarp();
         if (++st == a.n_stages) {
           st = 0;
@@ -289,153 +488,21 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     const int ew = (static_cast<int>(warp) - 4) >> 2;
     const int eb = ew & 1;
     const int wq = static_cast<int>(warp) & 3;
-    const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
-    const int pprime = row / a.cout;
-    const int c = row - pprime * a.cout;
-    const int phase = a.ph - 1 - pprime;
-    const int g8 = c >> 3;
-    const int r8 = static_cast<int>(lane) & 7;
-    const bool has_res = a.res_mode != 0 && g8 * 8 < a.res_c;
-    const int out_groups = a.cout / 8;
-    const int res_groups = a.res_c / 8;
-    const int nch = a.nb / 16;  // 16-column chunks of the tile; this warpgroup takes half (the first the larger)
-    const int c_lo = (ew >> 1) ? (nch + 1) / 2 : 0, c_hi = (ew >> 1) ? nch : (nch + 1) / 2;
+    const int c = (wq * 32 + static_cast<int>(lane)) & (a.cout - 1);
     for (int i = static_cast<int>(threadIdx.x) - 128; i < a.G * a.cout; i += kPPThreads - 128) {
       const int g = i / a.cout;
       s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
     }
     named_bar_sync(1, kPPThreads - 128);  // the epilogue warps alone: off the producer's path
     uint32_t accph = 0;
-    const bool eprof = (a.dbg & 16) && a.prof && warp == 4 && lane == 0;
-    unsigned long long e_wait = 0, e_work = 0, e_start = eprof ? clock64() : 0;
-    int e_tiles = 0;
     pdl_wait();
     const CtaRange cr = cta_range(a);
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
     for (int tile = cr.first + eb * cr.stride; tile < cr.end; tile += 2 * cr.stride) {
-      ++e_tiles;
       const PPTile t = pp_tile(a, tile);
-      const float bias = s_bias[t.g * a.cout + c];
-      const size_t out_plane = static_cast<size_t>(t.p) * out_groups + g8;
-      const size_t res_plane = static_cast<size_t>(t.p) * res_groups + g8;
-      const int n_base = t.nt * a.nb + r8;  // + 16*ch + 8*b: this lane's column after the transpose
-      float head = 0.f;
-      float fc8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) fc8[k] = a.fc_w ? a.fc_w[static_cast<size_t>(t.g) * a.cout + g8 * 8 + k] : 0.f;
-      // Shortcut rows of a chunk (2 positions per lane after the transpose;
-      // maxpool reads 2 rows each) are loaded two chunks ahead through two
-      // register sets (the chunk loop is unrolled by two so both stay in
-      // registers), the first two before the accumulator wait.
-      uint4 rawA[4], rawB[4];
-      const bool cg = (a.dbg & 64) != 0;
-      auto ldres = [&](const uint4* p) { return ldres_sel(p, cg); };
-      auto load_res = [&](int ch, uint4 (&raw)[4]) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int l = a.ph * (n_base + 16 * ch + 8 * b) + phase;
-          const bool ok = has_res && l < a.lout && !(a.dbg & 32);
-          const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-          if (a.res_mode == 2) {
-            raw[2 * b] = ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l))) : z;
-            raw[2 * b + 1] =
-                ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, 2 * l + 1))) : z;
-          } else {
-            raw[2 * b] = ok ? ldres(reinterpret_cast<const uint4*>(a.res + q_off(res_plane, a.res_qs, a.res_lq, l))) : z;
-          }
-        }
-      };
-      if (a.res_mode) {
-        load_res(c_lo, rawA);
-        if (c_lo + 1 < c_hi) load_res(c_lo + 1, rawB);
-      }
-      unsigned long long e0 = eprof ? clock64() : 0;
-      mbar_wait(&acc_full[eb], accph, 120);
-      tc_fence_after();
-      if (eprof) {
-        const unsigned long long e1 = clock64();
-        e_wait += e1 - e0;
-        e0 = e1;
-      }
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
-      auto chunk = [&](int ch, uint4 (&raw)[4]) {
-        uint32_t r[16];
-        tmem_ld16_nw(taddr + static_cast<uint32_t>(ch * 16), r);
-        uint4 rv[2];
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          if (a.res_mode == 2) {
-            const __half2* h0 = reinterpret_cast<const __half2*>(&raw[2 * b]);
-            const __half2* h1 = reinterpret_cast<const __half2*>(&raw[2 * b + 1]);
-            __half2* o2 = reinterpret_cast<__half2*>(&rv[b]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) o2[k] = __hmax2(h0[k], h1[k]);
-          } else {
-            rv[b] = a.res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
-          }
-        }
-        if (a.res_mode && ch + 2 < c_hi) load_res(ch + 2, raw);
-        tmem_wait_ld();
-        if (ch == c_hi - 1) {  // this warpgroup's columns drained
-          tc_fence_before();
-          mbar_arrive(&acc_empty[eb]);
-        }
-        if (a.dbg & 1) return;
-        // (acc + bias) is rounded to fp16 before the transpose; the shortcut
-        // add and ReLU run on half2 (two roundings instead of one: within one
-        // fp16 ulp of the fp32 reference, tests/test_conv_pp_gpu.py).
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          uint32_t h[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const __half2 v2 = __floats2half2_rn(__uint_as_float(r[8 * b + 2 * k]) + bias,
-                                                 __uint_as_float(r[8 * b + 2 * k + 1]) + bias);
-            h[k] = *reinterpret_cast<const uint32_t*>(&v2);
-          }
-          transpose8_h2(h, r8);
-          const int l = a.ph * (n_base + 16 * ch + 8 * b) + phase;
-          if (l < a.out_rows) {
-            const __half2* rr = reinterpret_cast<const __half2*>(&rv[b]);
-            const __half2 zero = __float2half2_rn(0.f);
-            const bool valid = l < a.lout;
-            uint4 pk;
-            __half2* o2 = reinterpret_cast<__half2*>(&pk);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const __half2 y = __hmax2(__hadd2(*reinterpret_cast<const __half2*>(&h[k]), rr[k]), zero);
-              o2[k] = valid ? y : zero;
-            }
-            if (a.fc_w == nullptr) {
-              *reinterpret_cast<uint4*>(a.out + q_off(out_plane, a.out_qs, a.out_lq, l)) = pk;
-            } else if (valid) {  // fused head: this position's 8 channels . fc
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const float2 f = __half22float2(o2[k]);
-                head = fmaf(f.x, fc8[2 * k], fmaf(f.y, fc8[2 * k + 1], head));
-              }
-            }
-          }
-        }
-      };
-      for (int ch = c_lo; ch < c_hi; ch += 2) {
-        chunk(ch, rawA);
-        if (ch + 1 < c_hi) chunk(ch + 1, rawB);
-      }
-      if (a.fc_w != nullptr) {  // one partial per (tile, epilogue warp), summed in fixed order by K5
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) head += __shfl_xor_sync(0xffffffffu, head, off);
-        if (lane == 0)
-          a.head_out[static_cast<size_t>(t.g) * a.head_g_stride + static_cast<size_t>(t.p - t.g * a.Pm) * a.head_mt +
-                     static_cast<size_t>(t.nt) * 8 + (ew >> 1) * 4 + wq] = head;  // (column half, warp)
-      }
-      if (eprof) e_work += clock64() - e0;
+      pp_epi_tile<false>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb],
+                         s_bias[t.g * a.cout + c], (a.dbg & 64) != 0, (a.dbg & 1) != 0);
       accph ^= 1u;
-    }
-    if (eprof) {
-      a.prof[blockIdx.x * 8 + 3] = e_wait;
-      a.prof[blockIdx.x * 8 + 4] = e_work;
-      a.prof[blockIdx.x * 8 + 5] = clock64() - e_start;
-      a.prof[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(e_tiles);
     }
   }
 
@@ -443,6 +510,326 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, a.tmem_cols);
+}
+
+// ------------------------------------------------------------------ K4c: chain
+// A whole member-group chain of K4b layers (and several chains side by side)
+// in ONE persistent launch.  Every CTA walks its own list of (layer, tile)
+// items, layer-major; a tile of layer j starts as soon as the tiles of its
+// producer layers that cover its input rows (and shortcut rows) are written,
+// tracked by per-tile counters in global memory, instead of at a grid-wide
+// kernel boundary.  Per item the three roles are those of conv_pp_kernel;
+// what changes:
+//  * the layer descriptors live in the parameter block (ChainArgs::L, read
+//    with uniform constant-bank loads) and the tensor maps in global memory;
+//  * the weight image is reloaded when the (layer, member) of the next item
+//    differs (MMA -> producer handshake w_empty / w_full, as a group change in
+//    conv_pp_kernel); the stage ring restarts at slot 0 there because the
+//    stage region begins right after the new image, and per-slot barrier
+//    phases are tracked as bit masks so a layer with fewer or more stages
+//    keeps both roles in step;
+//  * accumulators sit at fixed TMEM offsets (0 / 256), bias and FC weights
+//    are read from global (L1) per tile;
+//  * after its stores, each column half of a tile publishes itself: named
+//    barrier of its warpgroup, proxy fence, release add of 1 to the tile's
+//    counter.  The producer thread acquires every counter its next TMA boxes
+//    depend on (target 2 * (epoch + 1): counters only grow, `epoch` counts
+//    finished launches of this chain, bumped by the last CTA to exit), then
+//    issues a proxy fence and the loads.  The epilogue's shortcut rows are
+//    read through L2 (ld.global.cg): they are written inside this launch.
+// Deadlock freedom: each CTA's list is sorted by layer and a layer only waits
+// on lower layers, so by induction on the layer index every item completes
+// (the grid is at most one CTA per SM, all resident).
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_u32(unsigned* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Wait until every tile of chain layer `dl` covering output positions
+// [lo, hi) of row `row` has been published `target` times (both halves).
+__device__ __forceinline__ void chain_wait_range(const ChainArgs& ca, int dl, int row, long lo, long hi,
+                                                 uint32_t target) {
+  const PPArgs& d = ca.L[dl];
+  if (lo < 0) lo = 0;
+  if (hi > d.out_rows) hi = d.out_rows;
+  if (hi <= lo) return;
+  const long ppt = static_cast<long>(d.ph) * d.nb;
+  int t0 = static_cast<int>(lo / ppt), t1 = static_cast<int>((hi - 1) / ppt);
+  if (t1 >= d.nt_per_p) t1 = d.nt_per_p - 1;
+  const unsigned* f = ca.flags + ca.flag_base[dl] + static_cast<size_t>(row) * d.nt_per_p;
+  for (int t = t0; t <= t1; ++t) {
+    uint32_t n = 0;
+    while (static_cast<int>(ld_acquire_u32(f + t) - target) < 0) {
+      __nanosleep(64);
+      if (++n == (1u << 26)) asm volatile("trap;");  // a dependency that never lands is a planning bug
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_constant__ ChainArgs ca) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* st_full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* st_empty = st_full + kChainStages;
+  uint64_t* w_full = st_empty + kChainStages;
+  uint64_t* w_empty = w_full + 1;
+  uint64_t* acc_full = w_empty + 1;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint8_t* const sW = smem + kChainFixed;  // weight image, then the stage ring
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int i0 = ca.item_off[blockIdx.x], i1 = ca.item_off[blockIdx.x + 1];
+  auto item_layer = [&](int k) { return ca.items[k] >> 22; };
+  auto item_tile = [&](int k) { return ca.items[k] & ((1 << 22) - 1); };
+  // (layer, member) of an item: the weight image it needs
+  auto item_key = [&](int k) {
+    const int li = item_layer(k);
+    return li * kMaxGroup + pp_tile(ca.L[li], item_tile(k)).g;
+  };
+  auto load_w = [&](int key) {
+    const int li = key / kMaxGroup, g = key - li * kMaxGroup;
+    const PPArgs& a = ca.L[li];
+    const uint8_t* src = a.wimg + static_cast<size_t>(g) * a.w_stride;
+    mbar_arrive_expect_tx(w_full, a.w_bytes);
+    for (uint32_t off = 0; off < a.w_bytes; off += 32768u)
+      bulk_load(sW + off, src + off, (a.w_bytes - off) < 32768u ? (a.w_bytes - off) : 32768u, w_full);
+  };
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < kChainStages; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    mbar_init(w_full, 1);
+    mbar_init(w_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 256);
+    }
+    fence_barrier_init();
+    if (i0 < i1) load_w(item_key(i0));  // immutable: before the dependency wait
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------------------------------------------- producer
+      pdl_wait();
+      const bool prof = ca.prof != nullptr;
+      unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
+      const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
+      int cur_key = i0 < i1 ? item_key(i0) : -1, reloads = 0;
+      int st = 0;
+      uint32_t empty_ph = 0;  // per slot: parity of its uses so far
+      for (int k = i0; k < i1; ++k) {
+        const int li = item_layer(k), tile = item_tile(k);
+        const PPArgs& a = ca.L[li];
+        const PPTile t = pp_tile(a, tile);
+        const int key = li * kMaxGroup + t.g;
+        unsigned long long q0 = prof ? clock64() : 0;
+        if (key != cur_key) {  // next (layer, member): wait until the MMAs on the old image retired
+          mbar_wait(w_empty, static_cast<uint32_t>(reloads++) & 1u, 201);
+          if (prof) {
+            const unsigned long long q1 = clock64();
+            p_w += q1 - q0;
+            q0 = q1;
+          }
+          load_w(key);
+          cur_key = key;
+          st = 0;
+        }
+        const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
+        const long r0 = 8L * line0;
+        if (ca.dep_in[li] >= 0)
+          chain_wait_range(ca, ca.dep_in[li], t.p, a.Q * r0, a.Q * (r0 + a.R), target);
+        if (ca.dep_res[li] >= 0) {
+          const long ppt = static_cast<long>(a.ph) * a.nb;
+          if (a.n_res_pairs)  // shortcut rows as B stages: the same box in x's ph-phase layout
+            chain_wait_range(ca, ca.dep_res[li], t.p, a.ph * r0, a.ph * (r0 + a.R), target);
+          else if (a.res_mode == 1)
+            chain_wait_range(ca, ca.dep_res[li], t.p, ppt * t.nt, ppt * (t.nt + 1), target);
+          else if (a.res_mode == 2)
+            chain_wait_range(ca, ca.dep_res[li], t.p, 2 * ppt * t.nt, 2 * ppt * (t.nt + 1), target);
+        }
+        fence_proxy_async_global();
+        if (prof) {
+          const unsigned long long q1 = clock64();
+          p_dep += q1 - q0;
+          q0 = q1;
+        }
+        const CUtensorMap* tmB = ca.tmaps + 2 * li;
+        uint8_t* sB = sW + a.w_bytes;
+        const int planes_per_p = a.cin / 8;
+        for (int j = 0; j < a.n_pairs + a.n_res_pairs; ++j) {
+          mbar_wait(&st_empty[st], ((empty_ph >> st) & 1u) ^ 1u, 202);
+          if (prof) {
+            const unsigned long long q1 = clock64();
+            p_st += q1 - q0;
+            q0 = q1;
+          }
+          empty_ph ^= 1u << st;
+          mbar_arrive_expect_tx(&st_full[st], a.stage_bytes);
+          if (j < a.n_pairs)
+            tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, tmB, &st_full[st], 0, line0, 0,
+                        t.p * planes_per_p + 2 * j);
+          else
+            tma_load_4d(sB + static_cast<size_t>(st) * a.stage_bytes, tmB + 1, &st_full[st], 0, line0, 0,
+                        t.p * (a.res_c / 8) + 2 * (j - a.n_pairs));
+          if (++st == a.n_stages) st = 0;
+        }
+      }
+      if (prof) {
+        unsigned long long* pr = ca.prof + blockIdx.x * 16;
+        pr[0] = p_dep;
+        pr[1] = p_w;
+        pr[2] = p_st;
+        pr[3] = clock64() - p_start;
+        pr[4] = static_cast<unsigned long long>(i1 - i0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    int st = 0;
+    uint32_t full_ph = 0;
+    int acc = 0;
+    uint32_t accph = 0;
+    uint32_t wph = 0;
+    int cur_key = i0 < i1 ? item_key(i0) : -1;
+    const bool prof = ca.prof != nullptr && lane == 0;
+    unsigned long long m_w = 0, m_acc = 0, m_st = 0, m_start = prof ? clock64() : 0;
+    for (int k = i0; k < i1; ++k) {
+      const int li = item_layer(k);
+      const PPArgs& a = ca.L[li];
+      const PPTile t = pp_tile(a, item_tile(k));
+      const int key = li * kMaxGroup + t.g;
+      if (key != cur_key) {
+        wph ^= 1u;
+        cur_key = key;
+        st = 0;
+      }
+      unsigned long long q0 = prof ? clock64() : 0;
+      mbar_wait(w_full, wph, 211);
+      if (prof) {
+        const unsigned long long q1 = clock64();
+        m_w += q1 - q0;
+        q0 = q1;
+      }
+      mbar_wait(&acc_empty[acc], accph ^ 1u, 212);
+      if (prof) {
+        const unsigned long long q1 = clock64();
+        m_acc += q1 - q0;
+      }
+      tc_fence_after();
+      const uint32_t idesc = make_idesc_f16(kBM, a.nb);
+      const uint32_t b_lbo = static_cast<uint32_t>(a.Q * a.R * 16);
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+      const uint32_t sw = smem_u32(sW), sb = sw + a.w_bytes;
+      for (int j = 0; j < a.n_pairs + a.n_res_pairs; ++j) {
+        const unsigned long long q2 = prof ? clock64() : 0;
+        mbar_wait(&st_full[st], (full_ph >> st) & 1u, 213);
+        if (prof) m_st += clock64() - q2;
+        full_ph ^= 1u << st;
+        tc_fence_after();
+        const uint64_t b0 = make_desc(sb + static_cast<uint32_t>(st) * a.stage_bytes, b_lbo, 128);
+        if (elect_one()) {
+          if (j >= a.n_pairs) {
+            const uint64_t z0 = make_desc(sw + a.z_off + static_cast<uint32_t>(j - a.n_pairs) * a.z_pair_bytes,
+                                          a.z_half_bytes, 128);
+            for (int ps = 0; ps < a.ph; ++ps)
+              mma_f16_ss(d_tmem, z0 + static_cast<uint32_t>(ps * a.cout), b0 + static_cast<uint32_t>(ps * a.R + 8),
+                         idesc, 1u);
+            mma_commit(&st_empty[st]);
+          } else {
+            const uint64_t a0 = make_desc(sw + static_cast<uint32_t>(j) * a.w_pair_bytes, a.w_half_bytes, 128);
+            pp_issue_pair(a, d_tmem, a0, b0, idesc, j == 0, &st_empty[st]);
+          }
+        }
+        __syncwarp();
+        if (++st == a.n_stages) st = 0;
+      }
+      if (elect_one()) mma_commit(&acc_full[acc]);
+      __syncwarp();
+      if (k + 1 < i1 && item_key(k + 1) != key) {  // the weights change after this tile
+        if (elect_one()) mma_commit(w_empty);
+        __syncwarp();
+      }
+      if (++acc == 2) {
+        acc = 0;
+        accph ^= 1u;
+      }
+    }
+    if (prof) {
+      unsigned long long* pr = ca.prof + blockIdx.x * 16;
+      pr[5] = m_w;
+      pr[6] = m_acc;
+      pr[7] = m_st;
+      pr[8] = clock64() - m_start;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ epilogue
+    const int ew = (static_cast<int>(warp) - 4) >> 2;
+    const bool prof = ca.prof != nullptr && warp == 4 && lane == 0;
+    unsigned long long e_wait = 0, e_start = prof ? clock64() : 0;
+    const int eb = ew & 1;
+    const int wq = static_cast<int>(warp) & 3;
+    const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
+    const int r8 = static_cast<int>(lane) & 7;
+    uint32_t accph = 0;
+    pdl_wait();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * 256);
+    for (int k = i0 + eb; k < i1; k += 2) {
+      const int li = item_layer(k), tile = item_tile(k);
+      const PPArgs& a = ca.L[li];
+      const PPTile t = pp_tile(a, tile);
+      const int c = row & (a.cout - 1);
+      const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
+      const unsigned long long e0 = prof ? clock64() : 0;
+      // the shortcut rows are written inside this launch: read only once the
+      // accumulator is full (its MMAs ran on stages the producer loaded after
+      // acquiring this tile's dependencies), through L2
+      pp_epi_tile<true>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
+                        true, false);
+      if (prof) e_wait += clock64() - e0;
+      if (a.fc_w == nullptr) {  // publish this column half of the tile
+        named_bar_sync(2 + ew, 128);
+        if (wq == 0 && lane == 0) {
+          fence_proxy_async_global();
+          __threadfence();
+          red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
+        }
+      }
+      accph ^= 1u;
+    }
+    if (prof) {
+      unsigned long long* pr = ca.prof + blockIdx.x * 16;
+      pr[9] = e_wait;
+      pr[10] = clock64() - e_start;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+  if (threadIdx.x == 0) {  // the last CTA out advances the epoch (the next launch's counter target)
+    __threadfence();
+    if (atomicAdd(ca.sync + 1, 1u) == gridDim.x - 1) {
+      ca.sync[1] = 0u;
+      __threadfence();
+      atomicAdd(ca.sync, 1u);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -686,7 +1073,147 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
 }
 
 cudaError_t init_pp_kernel() {
-  return cudaFuncSetAttribute(conv_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  cudaError_t e = cudaFuncSetAttribute(conv_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(chain_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  return e;
+}
+
+void free_chain(ChainPlan* cp) {
+  cudaFree(cp->d_tmaps);
+  cudaFree(cp->d_items);
+  cudaFree(cp->d_item_off);
+  cudaFree(cp->d_flags);
+  cudaFree(cp->d_sync);
+  cudaFree(cp->d_prof);
+  delete cp->args;
+  *cp = ChainPlan();
+}
+
+// Work list of a chain launch.  The chains (member groups) get disjoint CTA
+// blocks in proportion to their MMA work (issued MMA columns per tile plus a
+// fixed per-tile term), so they run side by side with no barrier between
+// them.  Inside a block each layer's tiles are split by group member over
+// sub-blocks of CTAs (one weight image per CTA and layer), the member-to-
+// sub-block map rotating with the layer so no sub-block is always the short
+// one, round robin inside a sub-block; every CTA's list is layer-major.
+const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms) {
+  free_chain(cp);
+  if (n < 1 || n > kMaxChainLayers) return "chain: layer count out of range";
+  cp->args = new ChainArgs();
+  ChainArgs& ca = *cp->args;
+  std::memset(&ca, 0, sizeof(ca));
+  std::vector<CUtensorMap> tm(2 * n);
+  int n_chains = 0, flags = 0;
+  uint32_t smem = 0;
+  for (int i = 0; i < n; ++i) {
+    const PPPlan& p = *in[i].plan;
+    if (in[i].dep_in >= i || in[i].dep_res >= i) return "chain: a layer depends on a later one";
+    if (p.args.dbg) return "chain: debug knobs (HB_PP_DBG) are per-launch only";
+    ca.L[i] = p.args;
+    if (ca.L[i].n_stages > kChainStages) ca.L[i].n_stages = kChainStages;
+    ca.dep_in[i] = in[i].dep_in;
+    ca.dep_res[i] = in[i].dep_res;
+    ca.flag_base[i] = flags;
+    if (!p.args.fc_w) flags += p.args.num_tiles;
+    tm[2 * i] = p.tmap;
+    tm[2 * i + 1] = p.tmapX;
+    smem = std::max(smem, kChainFixed + p.args.w_bytes + static_cast<uint32_t>(ca.L[i].n_stages) * p.args.stage_bytes);
+    n_chains = std::max(n_chains, in[i].chain + 1);
+    if (p.args.num_tiles >= (1 << 22)) return "chain: too many tiles in one layer";
+  }
+  if (smem > kSmemLimit) return "chain: a layer does not fit in shared memory";
+  for (int i = 0; i < n; ++i) {  // a dependency must be on the same chain with the same row numbering
+    for (int d : {in[i].dep_in, in[i].dep_res})
+      if (d >= 0 && (in[d].chain != in[i].chain || ca.L[d].P != ca.L[i].P)) return "chain: bad dependency";
+  }
+  // CTA blocks per chain, proportional to the MMA work (largest remainder, >= 1 each)
+  std::vector<double> cost(n_chains, 0.0);
+  for (int i = 0; i < n; ++i) {
+    const PPArgs& a = ca.L[i];
+    const double mmas = a.n_pairs * a.U + a.n_res_pairs * a.ph;
+    cost[in[i].chain] += static_cast<double>(a.num_tiles) * (mmas * a.nb * 0.5 + 600.0);
+  }
+  const int grid = num_sms;
+  if (n_chains > grid) return "chain: more chains than SMs";
+  double tot = 0;
+  for (double v : cost) tot += v;
+  std::vector<int> ctas(n_chains, 1);
+  {
+    int left = grid - n_chains;
+    std::vector<std::pair<double, int>> rem;
+    for (int k = 0; k < n_chains; ++k) {
+      const double share = cost[k] / tot * grid - 1.0;
+      const int whole = std::max(0, std::min(left, static_cast<int>(share)));
+      ctas[k] += whole;
+      left -= whole;
+      rem.push_back({share - whole, k});
+    }
+    std::sort(rem.begin(), rem.end(), [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
+      return x.first > y.first;
+    });
+    for (size_t r = 0; left > 0; r = (r + 1) % rem.size(), --left) ctas[rem[r].second] += 1;
+  }
+  std::vector<std::vector<int>> lists(grid);
+  int base = 0;
+  for (int k = 0; k < n_chains; ++k) {
+    const int nb = ctas[k];
+    int layer_no = 0;
+    for (int i = 0; i < n; ++i) {
+      if (in[i].chain != k) continue;
+      const PPArgs& a = ca.L[i];
+      const int per_g = a.Pm * a.nt_per_p;
+      if (nb >= a.G) {
+        for (int g = 0; g < a.G; ++g) {
+          const int sb = (g + layer_no) % a.G;  // rotating member -> sub-block map
+          const int lo = (sb * nb) / a.G, hi = ((sb + 1) * nb) / a.G;
+          for (int j = 0; j < per_g; ++j) lists[base + lo + j % (hi - lo)].push_back((i << 22) | (g * per_g + j));
+        }
+      } else {
+        for (int t = 0; t < a.num_tiles; ++t) lists[base + t % nb].push_back((i << 22) | t);
+      }
+      ++layer_no;
+    }
+    base += nb;
+  }
+  std::vector<int> items, off(grid + 1, 0);
+  for (int b = 0; b < grid; ++b) {
+    off[b] = static_cast<int>(items.size());
+    items.insert(items.end(), lists[b].begin(), lists[b].end());
+  }
+  off[grid] = static_cast<int>(items.size());
+  auto cpy = [](void** dst, const void* src, size_t bytes) -> bool {
+    if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
+    return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (!cpy(reinterpret_cast<void**>(&cp->d_tmaps), tm.data(), sizeof(CUtensorMap) * tm.size()) ||
+      !cpy(reinterpret_cast<void**>(&cp->d_items), items.data(), sizeof(int) * std::max<size_t>(1, items.size())) ||
+      !cpy(reinterpret_cast<void**>(&cp->d_item_off), off.data(), sizeof(int) * off.size()))
+    return "chain: device allocation failed";
+  if (cudaMalloc(&cp->d_flags, sizeof(unsigned) * std::max(1, flags)) != cudaSuccess ||
+      cudaMemset(cp->d_flags, 0, sizeof(unsigned) * std::max(1, flags)) != cudaSuccess ||
+      cudaMalloc(&cp->d_sync, sizeof(unsigned) * 2) != cudaSuccess ||
+      cudaMemset(cp->d_sync, 0, sizeof(unsigned) * 2) != cudaSuccess)
+    return "chain: device allocation failed";
+  ca.tmaps = cp->d_tmaps;
+  ca.items = cp->d_items;
+  ca.item_off = cp->d_item_off;
+  ca.flags = cp->d_flags;
+  ca.sync = cp->d_sync;
+  if (getenv("HB_CHAIN_PROF") && atoi(getenv("HB_CHAIN_PROF"))) {
+    if (cudaMalloc(&cp->d_prof, sizeof(unsigned long long) * 16 * grid) != cudaSuccess ||
+        cudaMemset(cp->d_prof, 0, sizeof(unsigned long long) * 16 * grid) != cudaSuccess)
+      return "chain: device allocation failed";
+    ca.prof = cp->d_prof;
+  }
+  cp->grid = grid;
+  cp->n_layers = n;
+  cp->smem_bytes = smem;
+  return nullptr;
+}
+
+cudaError_t launch_chain(const ChainPlan& cp, cudaStream_t st) {
+  return launch_pdl(chain_pp_kernel, dim3(cp.grid), dim3(kPPThreads), cp.smem_bytes, st, *cp.args);
 }
 
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st) {

@@ -111,6 +111,7 @@ struct Group {
   int head_mt = 0;
   double flops = 0;
   std::vector<size_t> plan0;           // first plan index, per patient chunk
+  std::vector<__half*> cbuf;           // chain mode: output of every layer (0 = stem), one buffer each
 };
 
 struct Member {
@@ -175,6 +176,11 @@ struct hb_ctx {
   bool io_busy[2] = {false, false};
   int slot_M[2] = {0, 0};  // members of the tick submitted into each slot (its h_out layout)
   std::vector<LayerPlan> plans;
+  // K4c chain mode (HB_CHAIN): every group's K4b layers in one persistent launch
+  // with tile-level dependencies; each layer writes its own buffer (no reuse
+  // inside a tick, so no write-after-read hazard between tiles)
+  bool chain_on = false;
+  ChainPlan chain;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
   bool timed = false;
@@ -209,7 +215,10 @@ void free_selection(hb_ctx* c) {
   }
   for (auto& a : c->act) cudaFree(a);
   c->act.clear();
+  free_chain(&c->chain);
+  c->chain_on = false;
   for (auto& g : c->groups) {
+    for (auto p : g.cbuf) cudaFree(p);
     for (auto p : g.wpack) cudaFree(p);
     for (auto p : g.bias) cudaFree(p);
     cudaFree(g.fc_w);
@@ -241,7 +250,7 @@ void free_member(Member& m) {
 }
 
 // Kernel kinds reported by hb_profile_tick.
-enum { K_INGEST = 0, K_STEM = 1, K_CONV = 2, K_AGG = 3, K_ADV = 4, K_CONV_PP = 5 };
+enum { K_INGEST = 0, K_STEM = 1, K_CONV = 2, K_AGG = 3, K_ADV = 4, K_CONV_PP = 5, K_CHAIN = 6 };
 
 struct ProfRec {
   std::vector<cudaEvent_t>* ev = nullptr;  // event recorded after every launch
@@ -277,10 +286,23 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   // the aggregate (captured as parallel graph branches).  The eager profiling
   // path (pr->ev set) keeps everything on one stream so per-kernel event times
   // stay clean.
-  const bool fork = (pr->ev == nullptr) && c->lanes > 1;
+  if (c->chain_on) {  // stems, then every group's conv chain in one launch
+    for (const Group& g : c->groups) {
+      const int G = static_cast<int>(g.mi.size());
+      const double rows = static_cast<double>(c->Pc) * G;
+      const LayerSpec& s0 = g.layers[0];
+      CK(c, launch_stem(g.stem[0].data(), G, round_up(c->W, 8), c->Pc, c->W, layer_in_q(g.layers[1], g.kind[1]),
+                        s0.cout, s0.pad, g.cbuf[0], st));
+      pr->mark(st, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+    }
+    CK(c, launch_chain(c->chain, st));
+    pr->mark(st, K_CHAIN, c->chain.flops, c->chain.bytes);
+  }
+  const bool fork = !c->chain_on && (pr->ev == nullptr) && c->lanes > 1;
   if (fork) CK(c, cudaEventRecord(c->ev[0], st));
   std::vector<bool> lane_started(c->lanes, false);
   for (const Group& g : c->groups) {
+    if (c->chain_on) break;
     const int ln = g.lane;
     cudaStream_t ms = fork ? c->side[ln] : st;
     if (fork && !lane_started[ln]) {
@@ -373,8 +395,26 @@ int build_selection(hb_ctx* c) {
     for (size_t v : need) tot += 3.0 * v;
     return tot;
   };
+  for (auto& g : c->groups)
+    for (size_t li = 1; li < g.layers.size(); ++li) g.kind[li] = layer_kind(g.layers[li]);
+  {  // K4c chain mode: every conv of every group on K4b, one patient chunk, each layer its own buffer
+    static const int chain_env = getenv("HB_CHAIN") ? atoi(getenv("HB_CHAIN")) : 0;
+    bool ok = chain_env != 0;
+    double bytes = 0;
+    int n_layers = 0;
+    for (auto& g : c->groups)
+      for (size_t li = 0; li < g.layers.size(); ++li) {
+        const LayerSpec& L = g.layers[li];
+        if (li > 0) {
+          ok = ok && g.kind[li] == KIND_PP;
+          ++n_layers;
+        }
+        if (!L.head) bytes += static_cast<double>(c->P) * g.mi.size() * L.cout * plane_rows_max(L.lout) * sizeof(__half);
+      }
+    c->chain_on = ok && n_layers <= kMaxChainLayers && bytes <= c->act_budget;
+  }
   c->Pc = c->P;
-  while (c->Pc > 1 && size_for(c->Pc) > c->act_budget) c->Pc = (c->Pc + 1) / 2;
+  while (!c->chain_on && c->Pc > 1 && size_for(c->Pc) > c->act_budget) c->Pc = (c->Pc + 1) / 2;
   size_for(c->Pc);
   c->n_chunks = (c->P + c->Pc - 1) / c->Pc;
   c->P_pad = c->n_chunks * c->Pc;
@@ -384,7 +424,7 @@ int build_selection(hb_ctx* c) {
     CK(c, cudaMemset(c->xn, 0, xb));
   }
   c->act.assign(3 * c->lanes, nullptr);
-  for (int ln = 0; ln < c->lanes; ++ln)
+  for (int ln = 0; ln < c->lanes && !c->chain_on; ++ln)
     for (int k = 0; k < 3; ++k) {
       CK(c, cudaMalloc(&c->act[3 * ln + k], need[ln]));
       CK(c, cudaMemset(c->act[3 * ln + k], 0, need[ln]));
@@ -404,7 +444,16 @@ int build_selection(hb_ctx* c) {
   for (auto& g : c->groups) {
     const int G = static_cast<int>(g.mi.size());
     const int c_last = g.layers.back().cout;
-    for (size_t li = 1; li < g.layers.size(); ++li) g.kind[li] = layer_kind(g.layers[li]);
+    if (c->chain_on)
+      for (size_t li = 0; li + 1 < g.layers.size(); ++li) {
+        const LayerSpec& L = g.layers[li];
+        const size_t b = static_cast<size_t>(c->P) * G * L.cout * plane_rows_max(L.lout) * sizeof(__half);
+        __half* p = nullptr;
+        CK(c, cudaMalloc(&p, b));
+        CK(c, cudaMemset(p, 0, b));
+        g.cbuf.push_back(p);
+        c->act_bytes += b;
+      }
     // group-contiguous weight images (device-to-device from the registered members)
     for (size_t li = 1; li < g.layers.size(); ++li) {
       const LayerSpec& L = g.layers[li];
@@ -462,12 +511,14 @@ int build_selection(hb_ctx* c) {
         } else {
           src = (cur + 1) % 3;
           dst = (cur + 2) % 3;
-          res = act[cur];
+          res = c->chain_on ? g.cbuf[li - 2] : act[cur];
           res_len = g.layers[li - 1].lin;
           res_q = in_q(li - 1);  // the block input, as conv1 read it
           // the block output feeds the next block's conv1 in the layout that conv reads
           out_q = (li + 1 < g.layers.size()) ? in_q(li + 1) : 1;
         }
+        const __half* in_buf = c->chain_on ? g.cbuf[li - 1] : act[src];
+        __half* out_buf = L.head ? nullptr : (c->chain_on ? g.cbuf[li] : act[dst]);
         // head partials of chunk ch: rows [ch*Pc, (ch+1)*Pc) of every member's [P_pad][head_mt] block
         float* head_base = L.head ? g.head_partial + static_cast<size_t>(ch) * c->Pc * g.head_mt : nullptr;
         LayerPlan plan;
@@ -485,14 +536,14 @@ int build_selection(hb_ctx* c) {
         }
         const char* e;
         if (plan.kind == KIND_PP) {
-          e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
-                      L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
+          e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, in_buf,
+                      out_buf, out_q, g.wpack[li - 1], g.bias[li - 1], res,
                       conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, lane_sms, layer_zc(L),
                       L.head ? g.fc_w : nullptr, head_base, static_cast<size_t>(c->P_pad) * g.head_mt);
           if (!e && L.head && plan.pp.args.head_mt != g.head_mt) e = "conv_pp: head tiling mismatch";
         } else {
-          e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, act[src],
-                        L.head ? nullptr : act[dst], out_q, g.wpack[li - 1], g.bias[li - 1], res,
+          e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, in_buf,
+                        out_buf, out_q, g.wpack[li - 1], g.bias[li - 1], res,
                         conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, L.head ? g.fc_w : nullptr, head_base,
                         lane_sms, static_cast<size_t>(c->P_pad) * g.head_mt);
           if (!e && L.head && plan.tc.args.n_ntiles * plan.tc.args.mt_per_p != g.head_mt) e = "head tiling mismatch";
@@ -502,6 +553,31 @@ int build_selection(hb_ctx* c) {
         if (!conv1) cur = dst;
       }
     }
+  }
+  if (c->chain_on) {  // the chain's layer list: groups in order, layer-major; dependencies inside a group
+    std::vector<ChainLayerIn> cl;
+    double flops = 0, bytes = 0;
+    for (size_t gi = 0; gi < c->groups.size(); ++gi) {
+      const Group& g = c->groups[gi];
+      const int first = static_cast<int>(cl.size());
+      const double rows = static_cast<double>(c->P) * g.mi.size();
+      for (size_t li = 1; li < g.layers.size(); ++li) {
+        const LayerSpec& L = g.layers[li];
+        ChainLayerIn x;
+        x.plan = &c->plans[g.plan0[0] + li - 1].pp;
+        x.dep_in = li >= 2 ? first + static_cast<int>(li) - 2 : -1;
+        x.dep_res = (li % 2 == 0 && li >= 3) ? first + static_cast<int>(li) - 3 : -1;
+        x.chain = static_cast<int>(gi);
+        cl.push_back(x);
+        flops += rows * 2.0 * L.cin * L.cout * kTaps * L.lout;
+        bytes += rows * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
+                               (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0));
+      }
+    }
+    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), c->num_sms);
+    if (e) return fail(c, HB_E_INVALID, e);
+    c->chain.flops = flops;
+    c->chain.bytes = bytes;
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
   CK(c, cudaMemcpy(c->d_heads, heads.data(), sizeof(HeadMember) * heads.size(), cudaMemcpyHostToDevice));
@@ -933,6 +1009,16 @@ int hb_prepare(hb_ctx* c) {
   for (int k = 0; k < 2; ++k) CK(c, cudaGraphUpload(c->graph_io[k], c->own));
   CK(c, cudaStreamSynchronize(c->own));
   return HB_OK;
+}
+
+int hb_chain_profile(hb_ctx* c, unsigned long long* out, int cap) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  if (!c->chain_on || !c->chain.d_prof) return 0;
+  cudaSetDevice(c->device);
+  CK(c, cudaDeviceSynchronize());
+  const int n = std::min(cap, c->chain.grid);
+  if (out && n > 0) CK(c, cudaMemcpy(out, c->chain.d_prof, sizeof(unsigned long long) * 16 * n, cudaMemcpyDeviceToHost));
+  return c->chain.grid;
 }
 
 int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {

@@ -126,6 +126,42 @@ struct PPPlan {
   int grid;
   uint32_t smem_bytes;
 };
+// K4c: several member-group chains of K4b layers in one persistent launch
+// (conv_pp.cu: chain_pp_kernel).  Layer descriptors are in the parameter
+// block, tensor maps in global memory; per-tile counters order producer and
+// consumer tiles inside the launch.
+constexpr int kChainStages = 8;          // stage barriers (a layer uses its plan's n_stages <= this)
+constexpr uint32_t kChainFixed = 1024;   // barriers + TMEM holder, before the weight image
+constexpr int kMaxChainLayers = 36;
+struct ChainArgs {
+  PPArgs L[kMaxChainLayers];
+  int dep_in[kMaxChainLayers];     // chain layer writing this layer's input (-1: written before the launch)
+  int dep_res[kMaxChainLayers];    // chain layer writing its shortcut source (-1: none / before the launch)
+  int flag_base[kMaxChainLayers];  // first tile counter of the layer
+  const CUtensorMap* tmaps;        // [layer][2] (input view, shortcut view), global, 64-B aligned
+  const int* items;                // per CTA, layer-major: (layer << 22) | tile
+  const int* item_off;             // [grid + 1]
+  unsigned* flags;                 // tile counters (+2 per launch: two column halves)
+  unsigned* sync;                  // [0] finished launches (epoch), [1] CTAs out of the current launch
+  unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
+};
+struct ChainLayerIn {
+  const struct PPPlan* plan;
+  int dep_in, dep_res;
+  int chain;                       // independent sequence (a member group): CTAs are partitioned by chain
+};
+struct ChainPlan {
+  ChainArgs* args = nullptr;       // host copy of the parameter block
+  CUtensorMap* d_tmaps = nullptr;
+  int* d_items = nullptr;
+  int* d_item_off = nullptr;
+  unsigned* d_flags = nullptr;
+  unsigned* d_sync = nullptr;
+  unsigned long long* d_prof = nullptr;
+  int grid = 0, n_layers = 0;
+  uint32_t smem_bytes = 0;
+  double flops = 0, bytes = 0;     // algorithmic work per launch (set by the caller)
+};
 bool pp_shape_ok(int cin, int cout, int stride);
 int pp_phases(int cout);           // 128 / cout; the input of a pp conv is in Q = stride * phases layout
 // zc > 0: the image also carries the identity-shortcut selection arrays for zc
@@ -137,6 +173,9 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
                     const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc = 0,
                     const float* fc_w = nullptr, float* head_out = nullptr, size_t head_g_stride = 0);
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
+const char* plan_chain(ChainPlan* cp, const ChainLayerIn* layers, int n_layers, int num_sms);
+void free_chain(ChainPlan* cp);
+cudaError_t launch_chain(const ChainPlan& cp, cudaStream_t st);
 cudaError_t init_pp_kernel();
 
 // Build a plan (tensor map + tiling) for one conv layer.  The input layout is

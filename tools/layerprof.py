@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2008_04063_b200.engine import EnsembleEngine  # noqa: E402
 from paper_2008_04063_b200.zoo import Selector, holmes_zoo  # noqa: E402
 
-KIND = {0: "ingest+window", 1: "stem", 2: "conv K4", 3: "aggregate", 4: "advance", 5: "conv K4b"}
+KIND = {0: "ingest+window", 1: "stem", 2: "conv K4", 3: "aggregate", 4: "advance", 5: "conv K4b", 6: "chain K4c"}
 zoo = holmes_zoo()
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 idx = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [10, 13, 30, 50]
