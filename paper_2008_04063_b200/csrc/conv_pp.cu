@@ -552,24 +552,40 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Wait until every tile of chain layer `dl` covering output positions
-// [lo, hi) of row `row` has been published `target` times (both halves).
-__device__ __forceinline__ void chain_wait_range(const ChainArgs& ca, int dl, int row, long lo, long hi,
-                                                 uint32_t target) {
+// Tiles of chain layer `dl` covering output positions [lo, hi) of row `row`:
+// appended to the wait list (flag pointers), at most kMaxDeps in total.
+constexpr int kMaxDeps = 12;
+__device__ __forceinline__ void chain_dep_range(const ChainArgs& ca, int dl, int row, long lo, long hi,
+                                                const unsigned** list, int& n) {
   const PPArgs& d = ca.L[dl];
   if (lo < 0) lo = 0;
   if (hi > d.out_rows) hi = d.out_rows;
   if (hi <= lo) return;
   const long ppt = static_cast<long>(d.ph) * d.nb;
-  int t0 = static_cast<int>(lo / ppt), t1 = static_cast<int>((hi - 1) / ppt);
+  const int t0 = static_cast<int>(lo / ppt);
+  int t1 = static_cast<int>((hi - 1) / ppt);
   if (t1 >= d.nt_per_p) t1 = d.nt_per_p - 1;
   const unsigned* f = ca.flags + ca.flag_base[dl] + static_cast<size_t>(row) * d.nt_per_p;
-  for (int t = t0; t <= t1; ++t) {
-    uint32_t n = 0;
-    while (static_cast<int>(ld_acquire_u32(f + t) - target) < 0) {
-      __nanosleep(64);
-      if (++n == (1u << 26)) asm volatile("trap;");  // a dependency that never lands is a planning bug
-    }
+  for (int t = t0; t <= t1 && n < kMaxDeps; ++t) list[n++] = f + t;
+}
+// Wait until every listed counter reached `target`: all counters are read in
+// one batch (independent acquire loads, one L2 round trip), re-polling only
+// the ones still short.
+__device__ __forceinline__ void chain_wait_all(const unsigned** list, int n, uint32_t target) {
+  uint32_t v[kMaxDeps];
+  uint32_t spins = 0;
+  while (true) {
+#pragma unroll
+    for (int i = 0; i < kMaxDeps; ++i)
+      if (i < n) v[i] = ld_acquire_u32(list[i]);
+    int m = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxDeps; ++i)
+      if (i < n && static_cast<int>(v[i] - target) < 0) list[m++] = list[i];
+    n = m;
+    if (n == 0) return;
+    __nanosleep(64);
+    if (++spins == (1u << 26)) asm volatile("trap;");  // a dependency that never lands is a planning bug
   }
 }
 
@@ -578,21 +594,22 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   uint64_t* st_full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* st_empty = st_full + kChainStages;
   uint64_t* w_full = st_empty + kChainStages;
-  uint64_t* w_empty = w_full + 1;
-  uint64_t* acc_full = w_empty + 1;
+  uint64_t* acc_full = w_full + 1;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* it_full = acc_empty + 2;       // item ring: producer -> MMA + epilogue
+  uint64_t* it_empty = it_full + kChainRing;
+  int* ring = reinterpret_cast<int*>(it_empty + kChainRing);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ring + kChainRing);
   uint8_t* const sW = smem + kChainFixed;  // weight image, then the stage ring
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int i0 = ca.item_off[blockIdx.x], i1 = ca.item_off[blockIdx.x + 1];
-  auto item_layer = [&](int k) { return ca.items[k] >> 22; };
-  auto item_tile = [&](int k) { return ca.items[k] & ((1 << 22) - 1); };
+  auto item_layer = [](int it) { return it >> 22; };
+  auto item_tile = [](int it) { return it & ((1 << 22) - 1); };
   // (layer, member) of an item: the weight image it needs
-  auto item_key = [&](int k) {
-    const int li = item_layer(k);
-    return li * kMaxGroup + pp_tile(ca.L[li], item_tile(k)).g;
+  auto item_key = [&](int it) {
+    const int li = item_layer(it);
+    return li * kMaxGroup + pp_tile(ca.L[li], item_tile(it)).g;
   };
   auto load_w = [&](int key) {
     const int li = key / kMaxGroup, g = key - li * kMaxGroup;
@@ -602,19 +619,45 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     for (uint32_t off = 0; off < a.w_bytes; off += 32768u)
       bulk_load(sW + off, src + off, (a.w_bytes - off) < 32768u ? (a.w_bytes - off) : 32768u, w_full);
   };
+  // Next item of this CTA: its home chain's queue first, then (work stealing
+  // once that is drained) the other chains' queues in turn; -1 = all drained.
+  // The queue-head atomic is issued one item ahead (pull_issue) and resolved
+  // when the item is needed (pull_take), so its L2 round trip overlaps the
+  // current item's work instead of sitting on the producer's path.
+  int chain = ca.home[blockIdx.x], visited = 0;
+  unsigned pend = 0;
+  auto pull_issue = [&]() { pend = atomicAdd(ca.ctr + chain, 1u); };
+  auto pull_take = [&]() -> int {
+    while (visited < ca.n_chains) {
+      const int lo = ca.queue_off[chain], n = ca.queue_off[chain + 1] - lo;
+      if (static_cast<int>(pend) < n) return __ldg(ca.items + lo + pend);
+      chain = chain + 1 == ca.n_chains ? 0 : chain + 1;
+      if (++visited < ca.n_chains) pull_issue();
+    }
+    return -1;
+  };
+  auto pull = [&]() -> int {
+    pull_issue();
+    return pull_take();
+  };
+  int first = -1;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kChainStages; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 1);
     }
     mbar_init(w_full, 1);
-    mbar_init(w_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 256);
     }
+    for (int i = 0; i < kChainRing; ++i) {
+      mbar_init(&it_full[i], 1);
+      mbar_init(&it_empty[i], 1 + 256);  // the MMA warp + the two epilogue warpgroups of that parity
+    }
     fence_barrier_init();
-    if (i0 < i1) load_w(item_key(i0));  // immutable: before the dependency wait
+    first = pull();
+    if (first >= 0) load_w(item_key(first));  // immutable: before the dependency wait
   }
   if (warp == 2) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
@@ -629,17 +672,32 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
       const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
-      int cur_key = i0 < i1 ? item_key(i0) : -1, reloads = 0;
+      int cur_key = first >= 0 ? item_key(first) : -1;
       int st = 0;
-      uint32_t empty_ph = 0;  // per slot: parity of its uses so far
-      for (int k = i0; k < i1; ++k) {
-        const int li = item_layer(k), tile = item_tile(k);
+      uint32_t empty_ph = 0;  // per stage slot: parity of its uses so far
+      int it = first, seq = 0;
+      auto publish = [&](int value, int sq) {
+        const int slot = sq & (kChainRing - 1);
+        mbar_wait(&it_empty[slot], ((sq / kChainRing) & 1) ^ 1u, 200);
+        ring[slot] = value;
+        mbar_arrive(&it_full[slot]);
+      };
+      for (;; ++seq) {
+        if (seq > 0) it = pull_take();
+        if (it >= 0) pull_issue();  // the following item's queue head, resolved next iteration
+        publish(it, seq);
+        if (it < 0) {  // a second end mark for the other epilogue parity
+          publish(-1, seq + 1);
+          break;
+        }
+        const int li = item_layer(it), tile = item_tile(it);
         const PPArgs& a = ca.L[li];
         const PPTile t = pp_tile(a, tile);
         const int key = li * kMaxGroup + t.g;
         unsigned long long q0 = prof ? clock64() : 0;
-        if (key != cur_key) {  // next (layer, member): wait until the MMAs on the old image retired
-          mbar_wait(w_empty, static_cast<uint32_t>(reloads++) & 1u, 201);
+        if (key != cur_key) {  // next (layer, member): the previous item's MMAs must have retired
+          const int pv = seq - 1;
+          mbar_wait(&acc_full[pv & 1], static_cast<uint32_t>(pv >> 1) & 1u, 201);
           if (prof) {
             const unsigned long long q1 = clock64();
             p_w += q1 - q0;
@@ -651,16 +709,20 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         }
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
         const long r0 = 8L * line0;
-        if (ca.dep_in[li] >= 0)
-          chain_wait_range(ca, ca.dep_in[li], t.p, a.Q * r0, a.Q * (r0 + a.R), target);
-        if (ca.dep_res[li] >= 0) {
-          const long ppt = static_cast<long>(a.ph) * a.nb;
-          if (a.n_res_pairs)  // shortcut rows as B stages: the same box in x's ph-phase layout
-            chain_wait_range(ca, ca.dep_res[li], t.p, a.ph * r0, a.ph * (r0 + a.R), target);
-          else if (a.res_mode == 1)
-            chain_wait_range(ca, ca.dep_res[li], t.p, ppt * t.nt, ppt * (t.nt + 1), target);
-          else if (a.res_mode == 2)
-            chain_wait_range(ca, ca.dep_res[li], t.p, 2 * ppt * t.nt, 2 * ppt * (t.nt + 1), target);
+        {
+          const unsigned* deps[kMaxDeps];
+          int nd = 0;
+          if (ca.dep_in[li] >= 0) chain_dep_range(ca, ca.dep_in[li], t.p, a.Q * r0, a.Q * (r0 + a.R), deps, nd);
+          if (ca.dep_res[li] >= 0) {
+            const long ppt = static_cast<long>(a.ph) * a.nb;
+            if (a.n_res_pairs)  // shortcut rows as B stages: the same box in x's ph-phase layout
+              chain_dep_range(ca, ca.dep_res[li], t.p, a.ph * r0, a.ph * (r0 + a.R), deps, nd);
+            else if (a.res_mode == 1)
+              chain_dep_range(ca, ca.dep_res[li], t.p, ppt * t.nt, ppt * (t.nt + 1), deps, nd);
+            else if (a.res_mode == 2)
+              chain_dep_range(ca, ca.dep_res[li], t.p, 2 * ppt * t.nt, 2 * ppt * (t.nt + 1), deps, nd);
+          }
+          chain_wait_all(deps, nd, target);
         }
         fence_proxy_async_global();
         if (prof) {
@@ -695,7 +757,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         pr[1] = p_w;
         pr[2] = p_st;
         pr[3] = clock64() - p_start;
-        pr[4] = static_cast<unsigned long long>(i1 - i0);
+        pr[4] = static_cast<unsigned long long>(seq);
       }
     }
   } else if (warp == 1) {
@@ -705,16 +767,22 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     int acc = 0;
     uint32_t accph = 0;
     uint32_t wph = 0;
-    int cur_key = i0 < i1 ? item_key(i0) : -1;
+    int cur_key = -1;
     const bool prof = ca.prof != nullptr && lane == 0;
     unsigned long long m_w = 0, m_acc = 0, m_st = 0, m_start = prof ? clock64() : 0;
-    for (int k = i0; k < i1; ++k) {
-      const int li = item_layer(k);
+    for (int seq = 0;; ++seq) {
+      const int slot = seq & (kChainRing - 1);
+      mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 210);
+      const int it = ring[slot];
+      __syncwarp();
+      if (elect_one()) mbar_arrive(&it_empty[slot]);
+      if (it < 0) break;
+      const int li = item_layer(it);
       const PPArgs& a = ca.L[li];
-      const PPTile t = pp_tile(a, item_tile(k));
+      const PPTile t = pp_tile(a, item_tile(it));
       const int key = li * kMaxGroup + t.g;
       if (key != cur_key) {
-        wph ^= 1u;
+        if (cur_key >= 0) wph ^= 1u;
         cur_key = key;
         st = 0;
       }
@@ -760,10 +828,6 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       }
       if (elect_one()) mma_commit(&acc_full[acc]);
       __syncwarp();
-      if (k + 1 < i1 && item_key(k + 1) != key) {  // the weights change after this tile
-        if (elect_one()) mma_commit(w_empty);
-        __syncwarp();
-      }
       if (++acc == 2) {
         acc = 0;
         accph ^= 1u;
@@ -780,27 +844,30 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     // ------------------------------------------------------------------ epilogue
     const int ew = (static_cast<int>(warp) - 4) >> 2;
     const bool prof = ca.prof != nullptr && warp == 4 && lane == 0;
-    unsigned long long e_wait = 0, e_start = prof ? clock64() : 0;
+    unsigned long long e_work = 0, e_start = prof ? clock64() : 0;
     const int eb = ew & 1;
     const int wq = static_cast<int>(warp) & 3;
     const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
-    const int r8 = static_cast<int>(lane) & 7;
     uint32_t accph = 0;
     pdl_wait();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * 256);
-    for (int k = i0 + eb; k < i1; k += 2) {
-      const int li = item_layer(k), tile = item_tile(k);
+    for (int seq = eb;; seq += 2) {
+      const int slot = seq & (kChainRing - 1);
+      mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 219);
+      const int it = ring[slot];
+      mbar_arrive(&it_empty[slot]);
+      if (it < 0) break;
+      const int li = item_layer(it), tile = item_tile(it);
       const PPArgs& a = ca.L[li];
       const PPTile t = pp_tile(a, tile);
       const int c = row & (a.cout - 1);
       const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
-      const unsigned long long e0 = prof ? clock64() : 0;
       // the shortcut rows are written inside this launch: read only once the
       // accumulator is full (its MMAs ran on stages the producer loaded after
       // acquiring this tile's dependencies), through L2
       pp_epi_tile<true>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
                         true, false);
-      if (prof) e_wait += clock64() - e0;
+      const unsigned long long e0 = prof ? clock64() : 0;
       if (a.fc_w == nullptr) {  // publish this column half of the tile
         named_bar_sync(2 + ew, 128);
         if (wq == 0 && lane == 0) {
@@ -809,11 +876,12 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
         }
       }
+      if (prof) e_work += clock64() - e0;
       accph ^= 1u;
     }
     if (prof) {
       unsigned long long* pr = ca.prof + blockIdx.x * 16;
-      pr[9] = e_wait;
+      pr[9] = e_work;
       pr[10] = clock64() - e_start;
     }
   }
@@ -822,9 +890,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, 512);
-  if (threadIdx.x == 0) {  // the last CTA out advances the epoch (the next launch's counter target)
+  if (threadIdx.x == 0) {  // the last CTA out resets the queues and advances the epoch
     __threadfence();
     if (atomicAdd(ca.sync + 1, 1u) == gridDim.x - 1) {
+      for (int k = 0; k < ca.n_chains; ++k) ca.ctr[k] = 0u;
       ca.sync[1] = 0u;
       __threadfence();
       atomicAdd(ca.sync, 1u);
@@ -1090,13 +1159,13 @@ void free_chain(ChainPlan* cp) {
   *cp = ChainPlan();
 }
 
-// Work list of a chain launch.  The chains (member groups) get disjoint CTA
-// blocks in proportion to their MMA work (issued MMA columns per tile plus a
-// fixed per-tile term), so they run side by side with no barrier between
-// them.  Inside a block each layer's tiles are split by group member over
-// sub-blocks of CTAs (one weight image per CTA and layer), the member-to-
-// sub-block map rotating with the layer so no sub-block is always the short
-// one, round robin inside a sub-block; every CTA's list is layer-major.
+// Work of a chain launch: one queue per (chain, group member), layer-major,
+// tiles in (patient, column) order, pulled with an atomic counter.  Each CTA
+// has a home queue -- CTA blocks in proportion to the queues' MMA work
+// (issued MMA columns per tile plus a fixed per-tile term), so members run
+// side by side and a CTA changes weight image only at layer boundaries --
+// and steals from the other queues once its own is drained, which evens out
+// the cost model's error at the end of the launch.
 const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms) {
   free_chain(cp);
   if (n < 1 || n > kMaxChainLayers) return "chain: layer count out of range";
@@ -1127,77 +1196,86 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     for (int d : {in[i].dep_in, in[i].dep_res})
       if (d >= 0 && (in[d].chain != in[i].chain || ca.L[d].P != ca.L[i].P)) return "chain: bad dependency";
   }
-  // CTA blocks per chain, proportional to the MMA work (largest remainder, >= 1 each)
-  std::vector<double> cost(n_chains, 0.0);
-  for (int i = 0; i < n; ++i) {
-    const PPArgs& a = ca.L[i];
-    const double mmas = a.n_pairs * a.U + a.n_res_pairs * a.ph;
-    cost[in[i].chain] += static_cast<double>(a.num_tiles) * (mmas * a.nb * 0.5 + 600.0);
+  // One queue per (chain, group member): a member's layers use one weight
+  // image each, so a CTA drawing from one queue changes image only at layer
+  // boundaries.  CTA blocks per queue in proportion to the MMA work (largest
+  // remainder, >= 1 each).
+  std::vector<int> q_chain, q_member;
+  for (int k = 0; k < n_chains; ++k) {
+    int G = 0;
+    for (int i = 0; i < n; ++i)
+      if (in[i].chain == k) G = ca.L[i].G;
+    for (int g = 0; g < G; ++g) {
+      q_chain.push_back(k);
+      q_member.push_back(g);
+    }
   }
+  const int nq = static_cast<int>(q_chain.size());
+  std::vector<double> cost(nq, 0.0);
+  for (int q = 0; q < nq; ++q)
+    for (int i = 0; i < n; ++i) {
+      if (in[i].chain != q_chain[q]) continue;
+      const PPArgs& a = ca.L[i];
+      const double mmas = a.n_pairs * a.U + a.n_res_pairs * a.ph;
+      cost[q] += static_cast<double>(a.Pm * a.nt_per_p) * (mmas * a.nb * 0.5 + 600.0);
+    }
   const int grid = num_sms;
-  if (n_chains > grid) return "chain: more chains than SMs";
+  if (nq > grid) return "chain: more queues than SMs";
   double tot = 0;
   for (double v : cost) tot += v;
-  std::vector<int> ctas(n_chains, 1);
+  std::vector<int> ctas(nq, 1);
   {
-    int left = grid - n_chains;
+    int left = grid - nq;
     std::vector<std::pair<double, int>> rem;
-    for (int k = 0; k < n_chains; ++k) {
-      const double share = cost[k] / tot * grid - 1.0;
+    for (int q = 0; q < nq; ++q) {
+      const double share = cost[q] / tot * grid - 1.0;
       const int whole = std::max(0, std::min(left, static_cast<int>(share)));
-      ctas[k] += whole;
+      ctas[q] += whole;
       left -= whole;
-      rem.push_back({share - whole, k});
+      rem.push_back({share - whole, q});
     }
     std::sort(rem.begin(), rem.end(), [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
       return x.first > y.first;
     });
     for (size_t r = 0; left > 0; r = (r + 1) % rem.size(), --left) ctas[rem[r].second] += 1;
   }
-  std::vector<std::vector<int>> lists(grid);
-  int base = 0;
-  for (int k = 0; k < n_chains; ++k) {
-    const int nb = ctas[k];
-    int layer_no = 0;
+  // queue items: layer-major, the member's tiles in (patient, column) order
+  std::vector<int> items, qoff(nq + 1, 0), home(grid, 0);
+  for (int q = 0; q < nq; ++q) {
+    qoff[q] = static_cast<int>(items.size());
     for (int i = 0; i < n; ++i) {
-      if (in[i].chain != k) continue;
-      const PPArgs& a = ca.L[i];
-      const int per_g = a.Pm * a.nt_per_p;
-      if (nb >= a.G) {
-        for (int g = 0; g < a.G; ++g) {
-          const int sb = (g + layer_no) % a.G;  // rotating member -> sub-block map
-          const int lo = (sb * nb) / a.G, hi = ((sb + 1) * nb) / a.G;
-          for (int j = 0; j < per_g; ++j) lists[base + lo + j % (hi - lo)].push_back((i << 22) | (g * per_g + j));
-        }
-      } else {
-        for (int t = 0; t < a.num_tiles; ++t) lists[base + t % nb].push_back((i << 22) | t);
-      }
-      ++layer_no;
+      if (in[i].chain != q_chain[q]) continue;
+      const int per_g = ca.L[i].Pm * ca.L[i].nt_per_p;
+      for (int t = q_member[q] * per_g; t < (q_member[q] + 1) * per_g; ++t) items.push_back((i << 22) | t);
     }
-    base += nb;
   }
-  std::vector<int> items, off(grid + 1, 0);
-  for (int b = 0; b < grid; ++b) {
-    off[b] = static_cast<int>(items.size());
-    items.insert(items.end(), lists[b].begin(), lists[b].end());
+  qoff[nq] = static_cast<int>(items.size());
+  {
+    int b = 0;
+    for (int q = 0; q < nq; ++q)
+      for (int j = 0; j < ctas[q]; ++j) home[b++] = q;
   }
-  off[grid] = static_cast<int>(items.size());
   auto cpy = [](void** dst, const void* src, size_t bytes) -> bool {
     if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
     return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
+  std::vector<int> meta(qoff);  // [queue offsets (n_chains + 1)][home (grid)]
+  meta.insert(meta.end(), home.begin(), home.end());
   if (!cpy(reinterpret_cast<void**>(&cp->d_tmaps), tm.data(), sizeof(CUtensorMap) * tm.size()) ||
       !cpy(reinterpret_cast<void**>(&cp->d_items), items.data(), sizeof(int) * std::max<size_t>(1, items.size())) ||
-      !cpy(reinterpret_cast<void**>(&cp->d_item_off), off.data(), sizeof(int) * off.size()))
+      !cpy(reinterpret_cast<void**>(&cp->d_item_off), meta.data(), sizeof(int) * meta.size()))
     return "chain: device allocation failed";
   if (cudaMalloc(&cp->d_flags, sizeof(unsigned) * std::max(1, flags)) != cudaSuccess ||
       cudaMemset(cp->d_flags, 0, sizeof(unsigned) * std::max(1, flags)) != cudaSuccess ||
-      cudaMalloc(&cp->d_sync, sizeof(unsigned) * 2) != cudaSuccess ||
-      cudaMemset(cp->d_sync, 0, sizeof(unsigned) * 2) != cudaSuccess)
+      cudaMalloc(&cp->d_sync, sizeof(unsigned) * (2 + nq)) != cudaSuccess ||
+      cudaMemset(cp->d_sync, 0, sizeof(unsigned) * (2 + nq)) != cudaSuccess)
     return "chain: device allocation failed";
   ca.tmaps = cp->d_tmaps;
   ca.items = cp->d_items;
-  ca.item_off = cp->d_item_off;
+  ca.queue_off = cp->d_item_off;
+  ca.home = cp->d_item_off + nq + 1;
+  ca.n_chains = nq;
+  ca.ctr = cp->d_sync + 2;
   ca.flags = cp->d_flags;
   ca.sync = cp->d_sync;
   if (getenv("HB_CHAIN_PROF") && atoi(getenv("HB_CHAIN_PROF"))) {

@@ -131,7 +131,8 @@ struct PPPlan {
 // block, tensor maps in global memory; per-tile counters order producer and
 // consumer tiles inside the launch.
 constexpr int kChainStages = 8;          // stage barriers (a layer uses its plan's n_stages <= this)
-constexpr uint32_t kChainFixed = 1024;   // barriers + TMEM holder, before the weight image
+constexpr uint32_t kChainFixed = 1024;   // barriers, item ring, TMEM holder, before the weight image
+constexpr int kChainRing = 8;            // items in flight between the producer and the MMA / epilogue roles
 constexpr int kMaxChainLayers = 36;
 struct ChainArgs {
   PPArgs L[kMaxChainLayers];
@@ -139,8 +140,11 @@ struct ChainArgs {
   int dep_res[kMaxChainLayers];    // chain layer writing its shortcut source (-1: none / before the launch)
   int flag_base[kMaxChainLayers];  // first tile counter of the layer
   const CUtensorMap* tmaps;        // [layer][2] (input view, shortcut view), global, 64-B aligned
-  const int* items;                // per CTA, layer-major: (layer << 22) | tile
-  const int* item_off;             // [grid + 1]
+  const int* items;                // per queue ((chain, member) pair), layer-major: (layer << 22) | tile
+  const int* queue_off;            // [n_chains + 1]
+  const int* home;                 // [grid]: the queue a CTA drains first
+  int n_chains;                    // queues
+  unsigned* ctr;                   // [n_chains] queue heads (reset by the last CTA out)
   unsigned* flags;                 // tile counters (+2 per launch: two column halves)
   unsigned* sync;                  // [0] finished launches (epoch), [1] CTAs out of the current launch
   unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
@@ -154,7 +158,7 @@ struct ChainPlan {
   ChainArgs* args = nullptr;       // host copy of the parameter block
   CUtensorMap* d_tmaps = nullptr;
   int* d_items = nullptr;
-  int* d_item_off = nullptr;
+  int* d_item_off = nullptr;       // queue offsets, then home chains
   unsigned* d_flags = nullptr;
   unsigned* d_sync = nullptr;
   unsigned long long* d_prof = nullptr;
