@@ -594,7 +594,8 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   uint64_t* st_full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* st_empty = st_full + kChainStages;
   uint64_t* w_full = st_empty + kChainStages;
-  uint64_t* acc_full = w_full + 1;
+  uint64_t* w_empty = w_full + 1;
+  uint64_t* acc_full = w_empty + 1;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* it_full = acc_empty + 2;       // item ring: producer -> MMA + epilogue
   uint64_t* it_empty = it_full + kChainRing;
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       mbar_init(&st_empty[i], 1);
     }
     mbar_init(w_full, 1);
+    mbar_init(w_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 256);
@@ -672,7 +674,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
       const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
-      int cur_key = first >= 0 ? item_key(first) : -1;
+      int cur_key = first >= 0 ? item_key(first) : -1, reloads = 0;
       int st = 0;
       uint32_t empty_ph = 0;  // per stage slot: parity of its uses so far
       int it = first, seq = 0;
@@ -695,9 +697,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         const PPTile t = pp_tile(a, tile);
         const int key = li * kMaxGroup + t.g;
         unsigned long long q0 = prof ? clock64() : 0;
-        if (key != cur_key) {  // next (layer, member): the previous item's MMAs must have retired
-          const int pv = seq - 1;
-          mbar_wait(&acc_full[pv & 1], static_cast<uint32_t>(pv >> 1) & 1u, 201);
+        if (key != cur_key) {  // next (layer, member): wait until the MMAs on the old image retired
+          // (w_empty is committed by the MMA warp once per image change, so its
+          // phases cannot alias however far ahead this thread runs)
+          mbar_wait(w_empty, static_cast<uint32_t>(reloads++) & 1u, 201);
           if (prof) {
             const unsigned long long q1 = clock64();
             p_w += q1 - q0;
@@ -770,13 +773,16 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     int cur_key = -1;
     const bool prof = ca.prof != nullptr && lane == 0;
     unsigned long long m_w = 0, m_acc = 0, m_st = 0, m_start = prof ? clock64() : 0;
-    for (int seq = 0;; ++seq) {
-      const int slot = seq & (kChainRing - 1);
-      mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 210);
-      const int it = ring[slot];
+    auto read_item = [&](int sq) {
+      const int slot = sq & (kChainRing - 1);
+      mbar_wait(&it_full[slot], static_cast<uint32_t>(sq / kChainRing) & 1u, 210);
+      const int v = ring[slot];
       __syncwarp();
       if (elect_one()) mbar_arrive(&it_empty[slot]);
-      if (it < 0) break;
+      return v;
+    };
+    int it = read_item(0);
+    for (int seq = 0; it >= 0; ++seq) {
       const int li = item_layer(it);
       const PPArgs& a = ca.L[li];
       const PPTile t = pp_tile(a, item_tile(it));
@@ -828,6 +834,14 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       }
       if (elect_one()) mma_commit(&acc_full[acc]);
       __syncwarp();
+      // the next item (published before the producer's image wait): when it
+      // needs another image, release this one once these MMAs retire
+      const int nx = read_item(seq + 1);
+      if (nx >= 0 && item_key(nx) != key) {
+        if (elect_one()) mma_commit(w_empty);
+        __syncwarp();
+      }
+      it = nx;
       if (++acc == 2) {
         acc = 0;
         accph ^= 1u;
