@@ -1234,11 +1234,12 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
       cost[q] += static_cast<double>(a.Pm * a.nt_per_p) * (mmas * a.nb * 0.5 + 600.0);
     }
   const int grid = num_sms;
-  if (nq > grid) return "chain: more queues than SMs";
   double tot = 0;
   for (double v : cost) tot += v;
   std::vector<int> ctas(nq, 1);
-  {
+  if (nq > grid) {  // fewer CTAs than queues (a capped grid): one home each, the rest drained by stealing
+    for (int q = 0; q < nq; ++q) ctas[q] = q < grid ? 1 : 0;
+  } else {
     int left = grid - nq;
     std::vector<std::pair<double, int>> rem;
     for (int q = 0; q < nq; ++q) {

@@ -176,7 +176,7 @@ struct hb_ctx {
   bool io_busy[2] = {false, false};
   int slot_M[2] = {0, 0};  // members of the tick submitted into each slot (its h_out layout)
   std::vector<LayerPlan> plans;
-  // K4c chain mode (HB_CHAIN): every group's K4b layers in one persistent launch
+  // K4c chain mode (default; HB_CHAIN=0 disables): every group's K4b layers in one persistent launch
   // with tile-level dependencies; each layer writes its own buffer (no reuse
   // inside a tick, so no write-after-read hazard between tiles)
   bool chain_on = false;
@@ -398,8 +398,11 @@ int build_selection(hb_ctx* c) {
   for (auto& g : c->groups)
     for (size_t li = 1; li < g.layers.size(); ++li) g.kind[li] = layer_kind(g.layers[li]);
   {  // K4c chain mode: every conv of every group on K4b, one patient chunk, each layer its own buffer
-    static const int chain_env = getenv("HB_CHAIN") ? atoi(getenv("HB_CHAIN")) : 0;
-    bool ok = chain_env != 0;
+    // HB_CHAIN=0 keeps the per-layer launches (read per build, so tests can switch it); the
+    // per-launch debug knobs (HB_PP_DBG) exist only there
+    const char* ce = getenv("HB_CHAIN");
+    const char* dbg = getenv("HB_PP_DBG");
+    bool ok = (ce ? atoi(ce) : 1) != 0 && !(dbg && atoi(dbg));
     double bytes = 0;
     int n_layers = 0;
     for (auto& g : c->groups)
@@ -574,7 +577,9 @@ int build_selection(hb_ctx* c) {
                                (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0));
       }
     }
-    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), c->num_sms);
+    int grid = c->num_sms;  // HB_CHAIN_SMS caps the persistent grid (tests: many items per CTA, stealing)
+    if (const char* cs = getenv("HB_CHAIN_SMS")) grid = std::max(1, std::min(grid, atoi(cs)));
+    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), grid);
     if (e) return fail(c, HB_E_INVALID, e);
     c->chain.flops = flops;
     c->chain.bytes = bytes;

@@ -148,12 +148,35 @@ def test_window_alignment_and_warmup(hop):
 
 @pytest.mark.parametrize("lane_sms", ["3", "4", "6", "9"])
 def test_k4b_multi_tile_paths_forced(monkeypatch, lane_sms):
-    """Cap every conv grid at a few CTAs (HB_LANE_SMS) so that at 5 beds each persistent CTA
-    loops over many tiles: both TMEM accumulators and all four epilogue warpgroups, and either
-    member-partitioned CTAs (6, 9: the grid splits evenly over the 3-member group) or round-robin
-    CTAs that reload a different member's weight image mid-layer (3, 4)."""
+    """Per-layer K4b launches (HB_CHAIN=0) with every conv grid capped at a few CTAs
+    (HB_LANE_SMS) so that at 5 beds each persistent CTA loops over many tiles: both TMEM
+    accumulators and all four epilogue warpgroups, and either member-partitioned CTAs (6, 9: the
+    grid splits evenly over the 3-member group) or round-robin CTAs that reload a different
+    member's weight image mid-layer (3, 4)."""
+    monkeypatch.setenv("HB_CHAIN", "0")
     monkeypatch.setenv("HB_LANE_SMS", ",".join([lane_sms] * 4))
     _run(Selector.from_indices(60, C2), 5, 250, 2, 3, list(range(5)), xn_check=False)
+
+
+@pytest.mark.parametrize("chain_sms", ["1", "3", "5", "13"])
+def test_k4c_chain_capped_grid(monkeypatch, chain_sms):
+    """The K4c chain launch on a capped grid (HB_CHAIN_SMS): with fewer CTAs than queues every
+    queue but the home ones is drained by stealing (1, 3), and with a few CTAs per queue each CTA
+    walks many layers, weight images and dependency waits (5, 13) -- 7 beds, 2 sliding ticks,
+    every bed against the oracle."""
+    monkeypatch.setenv("HB_CHAIN", "1")
+    monkeypatch.setenv("HB_CHAIN_SMS", chain_sms)
+    _run(Selector.from_indices(60, C2), 7, 250, 2, 6, list(range(7)), xn_check=False)
+
+
+def test_k4c_chain_is_the_c2_tick():
+    """The benchmark's c2 selection runs as stems + ONE chain launch (kind 6) + the aggregate."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    zoo = holmes_zoo()
+    with EnsembleEngine(zoo, Selector.from_indices(60, C2), 8, hop=250) as eng:
+        eng.ingest(synth.ecg_block(0, 8, 3, 0, W))
+        kinds = eng.profile_tick()[0].tolist()
+    assert kinds == [0, 1, 1, 6, 3], kinds
 
 
 def test_k4b_group_caps(monkeypatch):
@@ -174,13 +197,16 @@ STATIC_KNOBS = [
     {"HB_WIN": "2"},                          # scalar register window kernel (pre-vectorisation)
     {"HB_WIN_NB": "3"},                       # TMA window kernel, 3 buffers (two streams of look-ahead)
     {"HB_WIN_NB": "1"},                       # TMA window kernel, 1 buffer (no look-ahead, 6 CTAs/SM)
+    {"HB_CHAIN": "0"},                        # per-layer K4b launches (lanes), no chain
+    {"HB_CHAIN": "0", "HB_PP_NB": "160"},     # per-layer, 160-wide tiles
+    {"HB_PP_STAGES": "6"},                    # chain: producer up to three items ahead of the MMA
 ]
 
 
 @pytest.mark.parametrize("env", STATIC_KNOBS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_k4b_planner_variants_match_oracle(tmp_path, env):
     """Planner knobs read once per process: run the tick in a subprocess and check its outputs
-    against the oracle (64 beds, c2 — the benchmark's shape)."""
+    against the oracle (64 beds, c2 — the benchmark's shape; the K4c chain unless HB_CHAIN=0)."""
     P, hop, ticks, seed = 64, 250, 2, 5
     out = tmp_path / "tick.npz"
     e = dict(os.environ, **env)

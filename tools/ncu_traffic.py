@@ -1,7 +1,8 @@
 """DRAM traffic of the conv kernels over one c2 tick, from an ncu CSV
 (--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
--k regex:conv_) -> profiles/ncu_conv_summary.json (read by bench.py): per
-kernel (K4b = conv_pp, K4 = conv_tc) and both together."""
+-k regex:"conv_|chain_") -> profiles/ncu_conv_summary.json (read by bench.py):
+per kernel (K4c = chain_pp, K4b = conv_pp, K4 = conv_tc) and the per-layer
+convs together."""
 import collections
 import csv
 import json
@@ -26,8 +27,10 @@ def summ(name):
 
 
 out = {"source": sys.argv[1], "note": "ncu serialises launches with cold caches; compare shares, not absolute times",
-       "conv_pp": summ("conv_pp"), "conv_tc": summ("conv_tc"), "all_conv": summ("conv_")}
-out.update(out["conv_pp"])  # the dominant kernel (K4b) at top level
+       "chain_pp": summ("chain_pp"), "conv_pp": summ("conv_pp"), "conv_tc": summ("conv_tc"),
+       "all_conv": summ("conv_")}
+# the dominant kernel at top level: the K4c chain launch when the tick ran it, else K4b
+out.update(out["chain_pp"] if out["chain_pp"]["launches"] else out["conv_pp"])
 if len(sys.argv) > 2:
     json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))
