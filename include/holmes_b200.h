@@ -139,6 +139,12 @@ int hb_prepare(hb_ctx* ctx);
  * accumulator-wait / total).  Returns the grid size (0 = no chain or no
  * profiling), copies min(grid, cap) rows. */
 int hb_chain_profile(hb_ctx* ctx, unsigned long long* out, int cap);
+/* Timeline of the last chain launch (same switches): per queue item, 5
+ * globaltimer ns values (pulled, its weight image in place, its dependencies
+ * met, each of its two column halves published), and the items themselves
+ * ((layer << 22) | tile).  Returns the item count (0 = off), copies
+ * min(count, cap) items. */
+int hb_chain_trace(hb_ctx* ctx, unsigned long long* trace, int* items, int cap);
 
 /* Diagnostics: raw gathered windows [P][n_leads][window] (fp32, host) and
  * (mean, std) [P][n_leads][2] of the most recent tick. */

@@ -55,6 +55,7 @@ _SIGS = {
     "hb_time_tick": (C.c_int, [_P, C.c_int, _F]),
     "hb_prepare": (C.c_int, [_P]),
     "hb_chain_profile": (C.c_int, [_P, C.c_void_p, C.c_int]),
+    "hb_chain_trace": (C.c_int, [_P, C.c_void_p, C.c_void_p, C.c_int]),
     "hb_device_sums": (C.c_int, [_P, C.POINTER(_P)]),
     "hb_finalize_sums": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     "hb_last_windows": (C.c_int, [_P, _F, _F, _P]),

@@ -540,6 +540,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 // Deadlock freedom: each CTA's list is sorted by layer and a layer only waits
 // on lower layers, so by induction on the layer index every item completes
 // (the grid is at most one CTA per SM, all resident).
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -565,8 +570,9 @@ __device__ __forceinline__ void chain_dep_range(const ChainArgs& ca, int dl, int
   const int t0 = static_cast<int>(lo / ppt);
   int t1 = static_cast<int>((hi - 1) / ppt);
   if (t1 >= d.nt_per_p) t1 = d.nt_per_p - 1;
-  const unsigned* f = ca.flags + ca.flag_base[dl] + static_cast<size_t>(row) * d.nt_per_p;
-  for (int t = t0; t <= t1 && n < kMaxDeps; ++t) list[n++] = f + t;
+  const int fs = ca.flag_stride;
+  const unsigned* f = ca.flags + ca.flag_base[dl] + static_cast<size_t>(row) * d.nt_per_p * fs;
+  for (int t = t0; t <= t1 && n < kMaxDeps; ++t) list[n++] = f + t * fs;
 }
 // Wait until every listed counter reached `target`: all counters are read in
 // one batch (independent acquire loads, one L2 round trip), re-polling only
@@ -628,10 +634,11 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   int chain = ca.home[blockIdx.x], visited = 0;
   unsigned pend = 0;
   auto pull_issue = [&]() { pend = atomicAdd(ca.ctr + chain, 1u); };
+  // returns the item's global queue index (items[gi] is the item), -1 when drained
   auto pull_take = [&]() -> int {
     while (visited < ca.n_chains) {
       const int lo = ca.queue_off[chain], n = ca.queue_off[chain + 1] - lo;
-      if (static_cast<int>(pend) < n) return __ldg(ca.items + lo + pend);
+      if (static_cast<int>(pend) < n) return lo + static_cast<int>(pend);
       chain = chain + 1 == ca.n_chains ? 0 : chain + 1;
       if (++visited < ca.n_chains) pull_issue();
     }
@@ -659,7 +666,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     }
     fence_barrier_init();
     first = pull();
-    if (first >= 0) load_w(item_key(first));  // immutable: before the dependency wait
+    if (first >= 0) load_w(item_key(__ldg(ca.items + first)));  // immutable: before the dependency wait
   }
   if (warp == 2) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
@@ -674,10 +681,11 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
       const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
-      int cur_key = first >= 0 ? item_key(first) : -1, reloads = 0;
+      int cur_key = first >= 0 ? item_key(__ldg(ca.items + first)) : -1, reloads = 0;
       int st = 0;
       uint32_t empty_ph = 0;  // per stage slot: parity of its uses so far
-      int it = first, seq = 0;
+      int gi = first, seq = 0;
+      unsigned long long* trace = ca.trace;
       auto publish = [&](int value, int sq) {
         const int slot = sq & (kChainRing - 1);
         mbar_wait(&it_empty[slot], ((sq / kChainRing) & 1) ^ 1u, 200);
@@ -685,13 +693,15 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         mbar_arrive(&it_full[slot]);
       };
       for (;; ++seq) {
-        if (seq > 0) it = pull_take();
-        if (it >= 0) pull_issue();  // the following item's queue head, resolved next iteration
-        publish(it, seq);
-        if (it < 0) {  // a second end mark for the other epilogue parity
+        if (seq > 0) gi = pull_take();
+        if (gi >= 0) pull_issue();  // the following item's queue head, resolved next iteration
+        publish(gi, seq);
+        if (gi < 0) {  // a second end mark for the other epilogue parity
           publish(-1, seq + 1);
           break;
         }
+        if (trace) trace[5 * gi + 0] = globaltimer();
+        const int it = __ldg(ca.items + gi);
         const int li = item_layer(it), tile = item_tile(it);
         const PPArgs& a = ca.L[li];
         const PPTile t = pp_tile(a, tile);
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           cur_key = key;
           st = 0;
         }
+        if (trace) trace[5 * gi + 1] = globaltimer();
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
         const long r0 = 8L * line0;
         {
@@ -727,7 +738,8 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           }
           chain_wait_all(deps, nd, target);
         }
-        fence_proxy_async_global();
+        if (trace) trace[5 * gi + 2] = globaltimer();
+        if (!(ca.opts & 1)) fence_proxy_async_global();
         if (prof) {
           const unsigned long long q1 = clock64();
           p_dep += q1 - q0;
@@ -781,8 +793,9 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       if (elect_one()) mbar_arrive(&it_empty[slot]);
       return v;
     };
-    int it = read_item(0);
-    for (int seq = 0; it >= 0; ++seq) {
+    int gi = read_item(0);
+    for (int seq = 0; gi >= 0; ++seq) {
+      const int it = __ldg(ca.items + gi);
       const int li = item_layer(it);
       const PPArgs& a = ca.L[li];
       const PPTile t = pp_tile(a, item_tile(it));
@@ -837,11 +850,11 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       // the next item (published before the producer's image wait): when it
       // needs another image, release this one once these MMAs retire
       const int nx = read_item(seq + 1);
-      if (nx >= 0 && item_key(nx) != key) {
+      if (nx >= 0 && item_key(__ldg(ca.items + nx)) != key) {
         if (elect_one()) mma_commit(w_empty);
         __syncwarp();
       }
-      it = nx;
+      gi = nx;
       if (++acc == 2) {
         acc = 0;
         accph ^= 1u;
@@ -868,9 +881,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     for (int seq = eb;; seq += 2) {
       const int slot = seq & (kChainRing - 1);
       mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 219);
-      const int it = ring[slot];
+      const int gi = ring[slot];
       mbar_arrive(&it_empty[slot]);
-      if (it < 0) break;
+      if (gi < 0) break;
+      const int it = __ldg(ca.items + gi);
       const int li = item_layer(it), tile = item_tile(it);
       const PPArgs& a = ca.L[li];
       const PPTile t = pp_tile(a, tile);
@@ -887,9 +901,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         if (wq == 0 && lane == 0) {
           fence_proxy_async_global();
           __threadfence();
-          red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
+          red_release_add_u32(ca.flags + ca.flag_base[li] + static_cast<size_t>(tile) * ca.flag_stride, 1u);
         }
       }
+      if (ca.trace && wq == 0 && lane == 0) ca.trace[5 * gi + 3 + (ew >> 1)] = globaltimer();
       if (prof) e_work += clock64() - e0;
       accph ^= 1u;
     }
@@ -1002,16 +1017,17 @@ static EncodeTiledFnPP get_encode_pp() {
 // partials, so it is chosen from the layer shape alone (the same model with the
 // wave quantisation dropped, i.e. as if the batch were large).  A bed's logit
 // is then bit-identical whatever the batch size, shard or grid cap.  HB_PP_NB
-// forces a width wherever it fits (elsewhere the model chooses).
+// forces a width wherever it fits (elsewhere the model chooses).  The knobs
+// are read per plan (tools/abtick.py compares settings in one process).
 static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::function<bool(int)>& fits,
                    bool maxpool_epi, bool shape_only) {
-  static const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
-  static const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
-  static const double fixed_cols = getenv("HB_PP_NB_FIXED") ? atof(getenv("HB_PP_NB_FIXED")) : 171.0;
+  const int force = getenv("HB_PP_NB") ? atoi(getenv("HB_PP_NB")) : 0;
+  const bool pow2_only = getenv("HB_PP_NB_POW2") && atoi(getenv("HB_PP_NB_POW2"));
+  const double fixed_cols = getenv("HB_PP_NB_FIXED") ? atof(getenv("HB_PP_NB_FIXED")) : 171.0;
   // maxpool shortcut in the epilogue at ph >= 4: the epilogue, not the MMA, sets
   // the pace and narrower tiles overlap it better (tools/nb_sweep.py: 160-wide
   // tiles 8-14 % faster on the 32-channel maxpool layers) - a smaller fixed term
-  static const double fixed_mp = getenv("HB_PP_NB_FIXED_MP") ? atof(getenv("HB_PP_NB_FIXED_MP")) : 60.0;
+  const double fixed_mp = getenv("HB_PP_NB_FIXED_MP") ? atof(getenv("HB_PP_NB_FIXED_MP")) : 60.0;
   if (force >= 64 && force <= 256 && force % 16 == 0 && fits(force)) return force;
   const double fixed = maxpool_epi ? fixed_mp : fixed_cols;
   int best = 0;
@@ -1034,7 +1050,7 @@ static int pick_nb(int tiles_per_col_unit, int n_cols, int num_sms, const std::f
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
                     const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc,
-                    const float* fc_w, float* head_out, size_t head_g_stride) {
+                    const float* fc_w, float* head_out, size_t head_g_stride, int prefer_nb) {
   std::memset(plan, 0, sizeof(*plan));
   if (G < 1 || G > kMaxGroup || Pm < 1) return "conv_pp: bad group shape";
   if (!pp_shape_ok(cin, cout, stride)) return "conv_pp: unsupported layer shape";
@@ -1087,13 +1103,15 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     const int R = round_up(8 + nb + dr_max, 8);
     return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
   };
-  a.nb = pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4, fc_w != nullptr);
+  a.nb = (prefer_nb >= 64 && prefer_nb <= 256 && prefer_nb % 16 == 0 && fits(prefer_nb) && !getenv("HB_PP_NB"))
+             ? prefer_nb
+             : pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4, fc_w != nullptr);
   if (!a.nb) return "conv_pp: no column tile fits in shared memory";
   a.R = round_up(8 + a.nb + dr_max, 8);
   a.stage_bytes = static_cast<uint32_t>(2 * a.Q * a.R * 16);
   a.n_stages = static_cast<int>(budget / a.stage_bytes);
   {
-    static const int cap = getenv("HB_PP_STAGES") ? atoi(getenv("HB_PP_STAGES")) : 4;
+    const int cap = getenv("HB_PP_STAGES") ? atoi(getenv("HB_PP_STAGES")) : 4;
     if (a.n_stages > cap) a.n_stages = cap;
   }
   a.nt_per_p = (n_cols + a.nb - 1) / a.nb;
@@ -1118,7 +1136,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   plan->smem_bytes = a.w_bytes + a.n_stages * a.stage_bytes + fixed;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
   {  // member-partitioned CTAs when that costs no extra wave (HB_PP_SPLIT=0 disables)
-    static const int split_on = getenv("HB_PP_SPLIT") ? atoi(getenv("HB_PP_SPLIT")) : 1;
+    const int split_on = getenv("HB_PP_SPLIT") ? atoi(getenv("HB_PP_SPLIT")) : 1;
     const int grid = plan->grid, per_g = a.Pm * a.nt_per_p;
     int waves_split = 0;
     for (int g = 0; g < G; ++g) {
@@ -1169,6 +1187,7 @@ void free_chain(ChainPlan* cp) {
   cudaFree(cp->d_flags);
   cudaFree(cp->d_sync);
   cudaFree(cp->d_prof);
+  cudaFree(cp->d_trace);
   delete cp->args;
   *cp = ChainPlan();
 }
@@ -1188,6 +1207,10 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
   std::memset(&ca, 0, sizeof(ca));
   std::vector<CUtensorMap> tm(2 * n);
   int n_chains = 0, flags = 0;
+  // HB_CHAIN_OPTS (experiments): 1 = no proxy fence on the consumer side, 2 = one 32-B sector per tile counter
+  ca.opts = getenv("HB_CHAIN_OPTS") ? atoi(getenv("HB_CHAIN_OPTS")) : 0;
+  const int fstride = (ca.opts & 2) ? 8 : 1;
+  ca.flag_stride = fstride;
   uint32_t smem = 0;
   for (int i = 0; i < n; ++i) {
     const PPPlan& p = *in[i].plan;
@@ -1198,7 +1221,7 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     ca.dep_in[i] = in[i].dep_in;
     ca.dep_res[i] = in[i].dep_res;
     ca.flag_base[i] = flags;
-    if (!p.args.fc_w) flags += p.args.num_tiles;
+    if (!p.args.fc_w) flags += p.args.num_tiles * fstride;
     tm[2 * i] = p.tmap;
     tm[2 * i + 1] = p.tmapX;
     smem = std::max(smem, kChainFixed + p.args.w_bytes + static_cast<uint32_t>(ca.L[i].n_stages) * p.args.stage_bytes);
@@ -1298,6 +1321,10 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
         cudaMemset(cp->d_prof, 0, sizeof(unsigned long long) * 16 * grid) != cudaSuccess)
       return "chain: device allocation failed";
     ca.prof = cp->d_prof;
+    if (cudaMalloc(&cp->d_trace, sizeof(unsigned long long) * 5 * std::max<size_t>(1, items.size())) != cudaSuccess)
+      return "chain: device allocation failed";
+    ca.trace = cp->d_trace;
+    cp->n_items = static_cast<int>(items.size());
   }
   cp->grid = grid;
   cp->n_layers = n;

@@ -61,15 +61,20 @@ bool pp_eligible(const LayerSpec& L) {
   return (heads || !L.head) && L.cin >= 16 && pp_shape_ok(L.cin, L.cout, L.stride);
 }
 // Head partials per patient of a K4b head layer (nt_per_p * 8), from a dry-run plan.
-int pp_head_mt(const LayerSpec& L, int G, int Pm, int sms) {
+int pp_head_mt(const LayerSpec& L, int G, int Pm, int sms, int prefer_nb = 0) {
   PPPlan plan;
   __half* fake = reinterpret_cast<__half*>(static_cast<uintptr_t>(1) << 20);  // encoded, never dereferenced
   const char* e = plan_pp(&plan, G, Pm, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, fake, nullptr, 1,
                           reinterpret_cast<uint8_t*>(fake), nullptr, L.res_mode ? fake : nullptr, L.res_mode, L.res_c,
                           L.res_mode == 2 ? 2 * L.lout : L.lout, L.res_mode == 2 ? 2 : 1, sms, 0,
-                          reinterpret_cast<const float*>(fake), reinterpret_cast<float*>(fake), 0);
+                          reinterpret_cast<const float*>(fake), reinterpret_cast<float*>(fake), 0, prefer_nb);
   return e ? -1 : plan.args.head_mt;
 }
+// Column tile of every K4c layer where it fits (HB_CHAIN_NB overrides): in one
+// persistent launch there are no per-layer waves to quantise, and the widest
+// tile measured fastest (tools/abtick.py: 256 vs the per-launch tile model -2 %,
+// vs 240 -0.4 %).
+int chain_nb() { return getenv("HB_CHAIN_NB") ? atoi(getenv("HB_CHAIN_NB")) : 256; }
 int layer_kind(const LayerSpec& L) {
   static const int pp_on = getenv("HB_PP") ? atoi(getenv("HB_PP")) : 1;
   return (pp_on && pp_eligible(L)) ? KIND_PP : KIND_TC;
@@ -478,7 +483,7 @@ int build_selection(hb_ctx* c) {
     {  // head partials per patient of the last layer, as that layer is tiled
       const LayerSpec& H = g.layers.back();
       if (g.kind.back() == KIND_PP) {
-        g.head_mt = pp_head_mt(H, G, c->Pc, c->num_sms);
+        g.head_mt = pp_head_mt(H, G, c->Pc, c->num_sms, c->chain_on ? chain_nb() : 0);
         if (g.head_mt <= 0) return fail(c, HB_E_INVALID, "conv_pp: head layer does not plan");
       } else {
         const int bn = conv_bn(H.cout), sm = conv_stride_m(conv_fold(H.cin, H.cout, H.stride));
@@ -542,7 +547,8 @@ int build_selection(hb_ctx* c) {
           e = plan_pp(&plan.pp, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, in_buf,
                       out_buf, out_q, g.wpack[li - 1], g.bias[li - 1], res,
                       conv1 ? 0 : L.res_mode, L.res_c, res_len, res_q, lane_sms, layer_zc(L),
-                      L.head ? g.fc_w : nullptr, head_base, static_cast<size_t>(c->P_pad) * g.head_mt);
+                      L.head ? g.fc_w : nullptr, head_base, static_cast<size_t>(c->P_pad) * g.head_mt,
+                      c->chain_on ? chain_nb() : 0);
           if (!e && L.head && plan.pp.args.head_mt != g.head_mt) e = "conv_pp: head tiling mismatch";
         } else {
           e = plan_conv(&plan.tc, G, c->Pc, L.cin, L.cout, L.lin, L.lout, L.stride, L.pad, in_buf,
@@ -1024,6 +1030,18 @@ int hb_chain_profile(hb_ctx* c, unsigned long long* out, int cap) {
   const int n = std::min(cap, c->chain.grid);
   if (out && n > 0) CK(c, cudaMemcpy(out, c->chain.d_prof, sizeof(unsigned long long) * 16 * n, cudaMemcpyDeviceToHost));
   return c->chain.grid;
+}
+
+int hb_chain_trace(hb_ctx* c, unsigned long long* trace, int* items, int cap) {
+  if (!c) return fail(c, HB_E_INVALID, "null argument");
+  if (!c->chain_on || !c->chain.d_trace) return 0;
+  cudaSetDevice(c->device);
+  CK(c, cudaDeviceSynchronize());
+  const int n = std::min(cap, c->chain.n_items);
+  if (trace && n > 0)
+    CK(c, cudaMemcpy(trace, c->chain.d_trace, sizeof(unsigned long long) * 5 * n, cudaMemcpyDeviceToHost));
+  if (items && n > 0) CK(c, cudaMemcpy(items, c->chain.d_items, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  return c->chain.n_items;
 }
 
 int hb_device_outputs(const hb_ctx* c, float** ml, float** ep, float** el) {

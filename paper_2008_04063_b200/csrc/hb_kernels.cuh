@@ -145,9 +145,13 @@ struct ChainArgs {
   const int* home;                 // [grid]: the queue a CTA drains first
   int n_chains;                    // queues
   unsigned* ctr;                   // [n_chains] queue heads (reset by the last CTA out)
-  unsigned* flags;                 // tile counters (+2 per launch: two column halves)
+  unsigned* flags;                 // tile counters (+2 per launch: two column halves), flag_stride apart
+  int flag_stride;
+  int opts;                        // HB_CHAIN_OPTS experiment bits
   unsigned* sync;                  // [0] finished launches (epoch), [1] CTAs out of the current launch
   unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
+  unsigned long long* trace;       // HB_CHAIN_PROF: per queue item [5] globaltimer ns: pulled, weights in place,
+                                   // dependencies met, column half 0 / 1 published
 };
 struct ChainLayerIn {
   const struct PPPlan* plan;
@@ -162,6 +166,8 @@ struct ChainPlan {
   unsigned* d_flags = nullptr;
   unsigned* d_sync = nullptr;
   unsigned long long* d_prof = nullptr;
+  unsigned long long* d_trace = nullptr;
+  int n_items = 0;
   int grid = 0, n_layers = 0;
   uint32_t smem_bytes = 0;
   double flops = 0, bytes = 0;     // algorithmic work per launch (set by the caller)
@@ -175,7 +181,8 @@ void pp_pack_weights(const float* w, int cin, int cout, int stride, uint16_t* ds
 const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int lout, int stride, int pad,
                     const __half* in, __half* out, int out_q, const uint8_t* wimg, const float* bias,
                     const __half* res, int res_mode, int res_c, int res_len, int res_q, int num_sms, int zc = 0,
-                    const float* fc_w = nullptr, float* head_out = nullptr, size_t head_g_stride = 0);
+                    const float* fc_w = nullptr, float* head_out = nullptr, size_t head_g_stride = 0,
+                    int prefer_nb = 0 /* column tile to use where it fits (K4c), 0 = the tile model */);
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
 const char* plan_chain(ChainPlan* cp, const ChainLayerIn* layers, int n_layers, int num_sms);
 void free_chain(ChainPlan* cp);
