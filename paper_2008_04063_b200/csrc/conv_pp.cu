@@ -1103,6 +1103,13 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     const int R = round_up(8 + nb + dr_max, 8);
     return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
   };
+  if (prefer_nb > 0) {
+    // K4c: narrower tiles for short layers, whose few tiles per bed otherwise
+    // leave a persistent CTA waiting on the previous layer's last tiles
+    // (HB_CHAIN_MIN_TILES: column tiles per bed below which the width halves)
+    const int min_tiles = getenv("HB_CHAIN_MIN_TILES") ? atoi(getenv("HB_CHAIN_MIN_TILES")) : 2;
+    while (prefer_nb > 64 && (n_cols + prefer_nb - 1) / prefer_nb < min_tiles) prefer_nb = round_up(prefer_nb / 2, 16);
+  }
   a.nb = (prefer_nb >= 64 && prefer_nb <= 256 && prefer_nb % 16 == 0 && fits(prefer_nb) && !getenv("HB_PP_NB"))
              ? prefer_nb
              : pick_nb(a.P, n_cols, num_sms, fits, res && res_mode == 2 && a.ph >= 4, fc_w != nullptr);
