@@ -557,23 +557,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Tiles of chain layer `dl` covering output positions [lo, hi) of row `row`:
-// appended to the wait list (flag pointers), at most kMaxDeps in total.
 constexpr int kMaxDeps = 12;
-__device__ __forceinline__ void chain_dep_range(const ChainArgs& ca, int dl, int row, long lo, long hi,
-                                                const unsigned** list, int& n) {
-  const PPArgs& d = ca.L[dl];
-  if (lo < 0) lo = 0;
-  if (hi > d.out_rows) hi = d.out_rows;
-  if (hi <= lo) return;
-  const long ppt = static_cast<long>(d.ph) * d.nb;
-  const int t0 = static_cast<int>(lo / ppt);
-  int t1 = static_cast<int>((hi - 1) / ppt);
-  if (t1 >= d.nt_per_p) t1 = d.nt_per_p - 1;
-  const int fs = ca.flag_stride;
-  const unsigned* f = ca.flags + ca.flag_base[dl] + static_cast<size_t>(row) * d.nt_per_p * fs;
-  for (int t = t0; t <= t1 && n < kMaxDeps; ++t) list[n++] = f + t * fs;
-}
 // Wait until every listed counter reached `target`: all counters are read in
 // one batch (independent acquire loads, one L2 round trip), re-polling only
 // the ones still short.
@@ -611,12 +595,12 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  auto item_layer = [](int it) { return it >> 22; };
-  auto item_tile = [](int it) { return it & ((1 << 22) - 1); };
-  // (layer, member) of an item: the weight image it needs
-  auto item_key = [&](int it) {
-    const int li = item_layer(it);
-    return li * kMaxGroup + pp_tile(ca.L[li], item_tile(it)).g;
+  // Queue item gi: idesc[gi] = {(layer << 22) | tile, bed row p, column tile nt, member g}
+  // (decoded on the host: this role's thread shares its sub-partition with four busy
+  // epilogue warps, so every instruction on its path is dear)
+  auto item_key = [&](int gi) {  // (layer, member): the weight image the item needs
+    const int4 d = __ldg(ca.idesc + gi);
+    return (d.x >> 22) * kMaxGroup + d.w;
   };
   auto load_w = [&](int key) {
     const int li = key / kMaxGroup, g = key - li * kMaxGroup;
@@ -666,7 +650,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     }
     fence_barrier_init();
     first = pull();
-    if (first >= 0) load_w(item_key(__ldg(ca.items + first)));  // immutable: before the dependency wait
+    if (first >= 0) load_w(item_key(first));  // immutable: before the dependency wait
   }
   if (warp == 2) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
@@ -681,7 +665,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
       const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
-      int cur_key = first >= 0 ? item_key(__ldg(ca.items + first)) : -1, reloads = 0;
+      int cur_key = first >= 0 ? item_key(first) : -1, reloads = 0;
       int st = 0;
       uint32_t empty_ph = 0;  // per stage slot: parity of its uses so far
       int gi = first, seq = 0;
@@ -701,10 +685,13 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           break;
         }
         if (trace) trace[5 * gi + 0] = globaltimer();
-        const int it = __ldg(ca.items + gi);
-        const int li = item_layer(it), tile = item_tile(it);
+        const int4 dsc = __ldg(ca.idesc + gi);
+        const int li = dsc.x >> 22;
         const PPArgs& a = ca.L[li];
-        const PPTile t = pp_tile(a, tile);
+        PPTile t;
+        t.p = dsc.y;
+        t.nt = dsc.z;
+        t.g = dsc.w;
         const int key = li * kMaxGroup + t.g;
         unsigned long long q0 = prof ? clock64() : 0;
         if (key != cur_key) {  // next (layer, member): wait until the MMAs on the old image retired
@@ -722,20 +709,12 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         }
         if (trace) trace[5 * gi + 1] = globaltimer();
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
-        const long r0 = 8L * line0;
-        {
+        {  // counters of the producer tiles this item's TMA boxes read (ranges decoded on the host)
+          const int4 dr = __ldg(ca.ideps + gi);
           const unsigned* deps[kMaxDeps];
           int nd = 0;
-          if (ca.dep_in[li] >= 0) chain_dep_range(ca, ca.dep_in[li], t.p, a.Q * r0, a.Q * (r0 + a.R), deps, nd);
-          if (ca.dep_res[li] >= 0) {
-            const long ppt = static_cast<long>(a.ph) * a.nb;
-            if (a.n_res_pairs)  // shortcut rows as B stages: the same box in x's ph-phase layout
-              chain_dep_range(ca, ca.dep_res[li], t.p, a.ph * r0, a.ph * (r0 + a.R), deps, nd);
-            else if (a.res_mode == 1)
-              chain_dep_range(ca, ca.dep_res[li], t.p, ppt * t.nt, ppt * (t.nt + 1), deps, nd);
-            else if (a.res_mode == 2)
-              chain_dep_range(ca, ca.dep_res[li], t.p, 2 * ppt * t.nt, 2 * ppt * (t.nt + 1), deps, nd);
-          }
+          for (int f = dr.x; f < dr.y; ++f) deps[nd++] = ca.flags + f;
+          for (int f = dr.z; f < dr.w; ++f) deps[nd++] = ca.flags + f;
           chain_wait_all(deps, nd, target);
         }
         if (trace) trace[5 * gi + 2] = globaltimer();
@@ -795,11 +774,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     };
     int gi = read_item(0);
     for (int seq = 0; gi >= 0; ++seq) {
-      const int it = __ldg(ca.items + gi);
-      const int li = item_layer(it);
+      const int4 dsc = __ldg(ca.idesc + gi);
+      const int li = dsc.x >> 22;
       const PPArgs& a = ca.L[li];
-      const PPTile t = pp_tile(a, item_tile(it));
-      const int key = li * kMaxGroup + t.g;
+      const int key = li * kMaxGroup + dsc.w;
       if (key != cur_key) {
         if (cur_key >= 0) wph ^= 1u;
         cur_key = key;
@@ -850,7 +828,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       // the next item (published before the producer's image wait): when it
       // needs another image, release this one once these MMAs retire
       const int nx = read_item(seq + 1);
-      if (nx >= 0 && item_key(__ldg(ca.items + nx)) != key) {
+      if (nx >= 0 && item_key(nx) != key) {
         if (elect_one()) mma_commit(w_empty);
         __syncwarp();
       }
@@ -884,10 +862,13 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const int gi = ring[slot];
       mbar_arrive(&it_empty[slot]);
       if (gi < 0) break;
-      const int it = __ldg(ca.items + gi);
-      const int li = item_layer(it), tile = item_tile(it);
+      const int4 dsc = __ldg(ca.idesc + gi);
+      const int li = dsc.x >> 22, tile = dsc.x & ((1 << 22) - 1);
       const PPArgs& a = ca.L[li];
-      const PPTile t = pp_tile(a, tile);
+      PPTile t;
+      t.p = dsc.y;
+      t.nt = dsc.z;
+      t.g = dsc.w;
       const int c = row & (a.cout - 1);
       const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
       // the shortcut rows are written inside this launch: read only once the
@@ -901,7 +882,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         if (wq == 0 && lane == 0) {
           fence_proxy_async_global();
           __threadfence();
-          red_release_add_u32(ca.flags + ca.flag_base[li] + static_cast<size_t>(tile) * ca.flag_stride, 1u);
+          red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
         }
       }
       if (ca.trace && wq == 0 && lane == 0) ca.trace[5 * gi + 3 + (ew >> 1)] = globaltimer();
@@ -1195,6 +1176,8 @@ void free_chain(ChainPlan* cp) {
   cudaFree(cp->d_sync);
   cudaFree(cp->d_prof);
   cudaFree(cp->d_trace);
+  cudaFree(cp->d_idesc);
+  cudaFree(cp->d_ideps);
   delete cp->args;
   *cp = ChainPlan();
 }
@@ -1214,10 +1197,8 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
   std::memset(&ca, 0, sizeof(ca));
   std::vector<CUtensorMap> tm(2 * n);
   int n_chains = 0, flags = 0;
-  // HB_CHAIN_OPTS (experiments): 1 = no proxy fence on the consumer side, 2 = one 32-B sector per tile counter
+  // HB_CHAIN_OPTS (experiments): 1 = no proxy fence on the consumer side
   ca.opts = getenv("HB_CHAIN_OPTS") ? atoi(getenv("HB_CHAIN_OPTS")) : 0;
-  const int fstride = (ca.opts & 2) ? 8 : 1;
-  ca.flag_stride = fstride;
   uint32_t smem = 0;
   for (int i = 0; i < n; ++i) {
     const PPPlan& p = *in[i].plan;
@@ -1228,7 +1209,7 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     ca.dep_in[i] = in[i].dep_in;
     ca.dep_res[i] = in[i].dep_res;
     ca.flag_base[i] = flags;
-    if (!p.args.fc_w) flags += p.args.num_tiles * fstride;
+    if (!p.args.fc_w) flags += p.args.num_tiles;
     tm[2 * i] = p.tmap;
     tm[2 * i + 1] = p.tmapX;
     smem = std::max(smem, kChainFixed + p.args.w_bytes + static_cast<uint32_t>(ca.L[i].n_stages) * p.args.stage_bytes);
@@ -1300,10 +1281,52 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     for (int q = 0; q < nq; ++q)
       for (int j = 0; j < ctas[q]; ++j) home[b++] = q;
   }
+  // per item: its decoded tile and the counters of the producer tiles its TMA boxes
+  // (input rows [Q(nt*nb - 8), Q(nt*nb - 8 + R)), shortcut rows) cover
+  std::vector<int4> idesc(items.size()), ideps(items.size());
+  auto dep_range = [&](int dl, int row, long lo, long hi, int* f0, int* f1) {
+    *f0 = *f1 = 0;
+    const PPArgs& d = ca.L[dl];
+    lo = std::max(lo, 0L);
+    hi = std::min(hi, static_cast<long>(d.out_rows));
+    if (hi <= lo) return;
+    const long ppt = static_cast<long>(d.ph) * d.nb;
+    const long t0 = lo / ppt, t1 = std::min((hi - 1) / ppt, static_cast<long>(d.nt_per_p - 1));
+    const int base = ca.flag_base[dl] + row * d.nt_per_p;
+    *f0 = base + static_cast<int>(t0);
+    *f1 = base + static_cast<int>(t1) + 1;
+  };
+  for (size_t k = 0; k < items.size(); ++k) {
+    const int i = items[k] >> 22, tile = items[k] & ((1 << 22) - 1);
+    const PPArgs& a = ca.L[i];
+    const int per_g = a.Pm * a.nt_per_p;
+    const int g = tile / per_g, rem = tile - g * per_g, pl = rem / a.nt_per_p, nt = rem - pl * a.nt_per_p;
+    const int p = g * a.Pm + pl;
+    idesc[k] = make_int4(items[k], p, nt, g);
+    int4 dr = make_int4(0, 0, 0, 0);
+    const long r0 = 8L * (nt * (a.nb / 8) - 1);
+    if (ca.dep_in[i] >= 0) dep_range(ca.dep_in[i], p, a.Q * r0, a.Q * (r0 + a.R), &dr.x, &dr.y);
+    if (ca.dep_res[i] >= 0) {
+      const long ppt = static_cast<long>(a.ph) * a.nb;
+      if (a.n_res_pairs)
+        dep_range(ca.dep_res[i], p, a.ph * r0, a.ph * (r0 + a.R), &dr.z, &dr.w);
+      else if (a.res_mode == 1)
+        dep_range(ca.dep_res[i], p, ppt * nt, ppt * (nt + 1), &dr.z, &dr.w);
+      else if (a.res_mode == 2)
+        dep_range(ca.dep_res[i], p, 2 * ppt * nt, 2 * ppt * (nt + 1), &dr.z, &dr.w);
+    }
+    if ((dr.y - dr.x) + (dr.w - dr.z) > kMaxDeps) return "chain: an item depends on too many tiles";
+    ideps[k] = dr;
+  }
   auto cpy = [](void** dst, const void* src, size_t bytes) -> bool {
     if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
     return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
   };
+  if (!cpy(reinterpret_cast<void**>(&cp->d_idesc), idesc.data(), sizeof(int4) * std::max<size_t>(1, idesc.size())) ||
+      !cpy(reinterpret_cast<void**>(&cp->d_ideps), ideps.data(), sizeof(int4) * std::max<size_t>(1, ideps.size())))
+    return "chain: device allocation failed";
+  ca.idesc = cp->d_idesc;
+  ca.ideps = cp->d_ideps;
   std::vector<int> meta(qoff);  // [queue offsets (n_chains + 1)][home (grid)]
   meta.insert(meta.end(), home.begin(), home.end());
   if (!cpy(reinterpret_cast<void**>(&cp->d_tmaps), tm.data(), sizeof(CUtensorMap) * tm.size()) ||

@@ -145,8 +145,9 @@ struct ChainArgs {
   const int* home;                 // [grid]: the queue a CTA drains first
   int n_chains;                    // queues
   unsigned* ctr;                   // [n_chains] queue heads (reset by the last CTA out)
-  unsigned* flags;                 // tile counters (+2 per launch: two column halves), flag_stride apart
-  int flag_stride;
+  const int4* idesc;               // per item: {(layer << 22) | tile, bed row, column tile, member}
+  const int4* ideps;               // per item: counter index ranges [x, y) (input) and [z, w) (shortcut)
+  unsigned* flags;                 // tile counters (+2 per launch: two column halves)
   int opts;                        // HB_CHAIN_OPTS experiment bits
   unsigned* sync;                  // [0] finished launches (epoch), [1] CTAs out of the current launch
   unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
@@ -167,6 +168,8 @@ struct ChainPlan {
   unsigned* d_sync = nullptr;
   unsigned long long* d_prof = nullptr;
   unsigned long long* d_trace = nullptr;
+  int4* d_idesc = nullptr;
+  int4* d_ideps = nullptr;
   int n_items = 0;
   int grid = 0, n_layers = 0;
   uint32_t smem_bytes = 0;

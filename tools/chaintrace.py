@@ -1,6 +1,6 @@
 """Per-layer timeline of one K4c chain launch (HB_CHAIN_PROF=1): for every chain
 layer, when its items were pulled / became ready / were published, and how
-long items waited for dependencies.  usage: python tools/chaintrace.py [P]"""
+long items waited for dependencies.  usage: python tools/chaintrace.py [P] [out.npz]"""
 import ctypes as C
 import os
 import sys
@@ -24,6 +24,8 @@ tr = np.zeros((cap, 5), np.uint64)
 items = np.zeros(cap, np.int32)
 n = _lib.lib().hb_chain_trace(eng._h, tr.ctypes.data_as(C.c_void_p), items.ctypes.data_as(C.c_void_p), cap)
 tr, items = tr[:n].astype(np.int64), items[:n]
+if len(sys.argv) > 2:
+    np.savez(sys.argv[2], trace=tr, items=items)
 t0 = tr[:, 0].min()
 pull, wdone, ready = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
 done = (np.maximum(tr[:, 3], tr[:, 4]) - t0) / 1e3
