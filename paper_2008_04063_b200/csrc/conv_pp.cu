@@ -557,23 +557,23 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-constexpr int kMaxDeps = 12;
-// Wait until every listed counter reached `target`: all counters are read in
-// one batch (independent acquire loads, one L2 round trip), re-polling only
-// the ones still short.
-__device__ __forceinline__ void chain_wait_all(const unsigned** list, int n, uint32_t target) {
-  uint32_t v[kMaxDeps];
+// Wait until the counters [a0, a1) and [b0, b1) (at most kMaxRange each) reached
+// `target`: all read in one batch of independent acquire loads (one L2 round
+// trip), registers only, re-polled with a short sleep while any is short.
+constexpr int kMaxRange = 6;
+__device__ __forceinline__ void chain_wait_ranges(const unsigned* flags, int a0, int a1, int b0, int b1,
+                                                  uint32_t target) {
   uint32_t spins = 0;
   while (true) {
+    uint32_t va[kMaxRange], vb[kMaxRange];
 #pragma unroll
-    for (int i = 0; i < kMaxDeps; ++i)
-      if (i < n) v[i] = ld_acquire_u32(list[i]);
-    int m = 0;
+    for (int k = 0; k < kMaxRange; ++k) va[k] = a0 + k < a1 ? ld_acquire_u32(flags + a0 + k) : target;
 #pragma unroll
-    for (int i = 0; i < kMaxDeps; ++i)
-      if (i < n && static_cast<int>(v[i] - target) < 0) list[m++] = list[i];
-    n = m;
-    if (n == 0) return;
+    for (int k = 0; k < kMaxRange; ++k) vb[k] = b0 + k < b1 ? ld_acquire_u32(flags + b0 + k) : target;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < kMaxRange; ++k) ok = ok && static_cast<int>(va[k] - target) >= 0 && static_cast<int>(vb[k] - target) >= 0;
+    if (ok) return;
     __nanosleep(64);
     if (++spins == (1u << 26)) asm volatile("trap;");  // a dependency that never lands is a planning bug
   }
@@ -711,11 +711,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
         {  // counters of the producer tiles this item's TMA boxes read (ranges decoded on the host)
           const int4 dr = __ldg(ca.ideps + gi);
-          const unsigned* deps[kMaxDeps];
-          int nd = 0;
-          for (int f = dr.x; f < dr.y; ++f) deps[nd++] = ca.flags + f;
-          for (int f = dr.z; f < dr.w; ++f) deps[nd++] = ca.flags + f;
-          chain_wait_all(deps, nd, target);
+          chain_wait_ranges(ca.flags, dr.x, dr.y, dr.z, dr.w, target);
         }
         if (trace) trace[5 * gi + 2] = globaltimer();
         if (!(ca.opts & 1)) fence_proxy_async_global();
@@ -1315,7 +1311,7 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
       else if (a.res_mode == 2)
         dep_range(ca.dep_res[i], p, 2 * ppt * nt, 2 * ppt * (nt + 1), &dr.z, &dr.w);
     }
-    if ((dr.y - dr.x) + (dr.w - dr.z) > kMaxDeps) return "chain: an item depends on too many tiles";
+    if (dr.y - dr.x > kMaxRange || dr.w - dr.z > kMaxRange) return "chain: an item depends on too many tiles";
     ideps[k] = dr;
   }
   auto cpy = [](void** dst, const void* src, size_t bytes) -> bool {
