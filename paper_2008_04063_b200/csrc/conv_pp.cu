@@ -616,14 +616,16 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   // when the item is needed (pull_take), so its L2 round trip overlaps the
   // current item's work instead of sitting on the producer's path.
   int chain = ca.home[blockIdx.x], visited = 0;
+  int q_lo = ca.queue_off[chain], q_n = ca.queue_off[chain + 1] - q_lo;  // the current queue's bounds
   unsigned pend = 0;
   auto pull_issue = [&]() { pend = atomicAdd(ca.ctr + chain, 1u); };
-  // returns the item's global queue index (items[gi] is the item), -1 when drained
+  // returns the item's global queue index (idesc[gi] describes it), -1 when drained
   auto pull_take = [&]() -> int {
     while (visited < ca.n_chains) {
-      const int lo = ca.queue_off[chain], n = ca.queue_off[chain + 1] - lo;
-      if (static_cast<int>(pend) < n) return lo + static_cast<int>(pend);
+      if (static_cast<int>(pend) < q_n) return q_lo + static_cast<int>(pend);
       chain = chain + 1 == ca.n_chains ? 0 : chain + 1;
+      q_lo = ca.queue_off[chain];
+      q_n = ca.queue_off[chain + 1] - q_lo;
       if (++visited < ca.n_chains) pull_issue();
     }
     return -1;
