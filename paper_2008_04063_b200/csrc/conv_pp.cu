@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* it_full = acc_empty + 2;       // item ring: producer -> MMA + epilogue
   uint64_t* it_empty = it_full + kChainRing;
-  int* ring = reinterpret_cast<int*>(it_empty + kChainRing);
+  uint64_t* it_ready = it_empty + kChainRing;  // the item's dependencies are met (its shortcut rows are readable)
+  int* ring = reinterpret_cast<int*>(it_ready + kChainRing);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ring + kChainRing);
   uint8_t* const sW = smem + kChainFixed;  // weight image, then the stage ring
 
@@ -649,6 +650,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     for (int i = 0; i < kChainRing; ++i) {
       mbar_init(&it_full[i], 1);
       mbar_init(&it_empty[i], 1 + 256);  // the MMA warp + the two epilogue warpgroups of that parity
+      mbar_init(&it_ready[i], 1);
     }
     fence_barrier_init();
     first = pull();
@@ -717,6 +719,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         }
         if (trace) trace[5 * gi + 2] = globaltimer();
         if (!(ca.opts & 1)) fence_proxy_async_global();
+        mbar_arrive(&it_ready[seq & (kChainRing - 1)]);  // the epilogue may now read this item's shortcut rows
         if (prof) {
           const unsigned long long q1 = clock64();
           p_dep += q1 - q0;
@@ -858,8 +861,12 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const int slot = seq & (kChainRing - 1);
       mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 219);
       const int gi = ring[slot];
-      mbar_arrive(&it_empty[slot]);
       if (gi < 0) break;
+      // the producer acquired this item's dependencies: its shortcut rows may be
+      // read ahead of the accumulator wait, as K4b does (the ring slot is released
+      // only after this wait, so it_ready's phases cannot alias)
+      mbar_wait(&it_ready[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 218);
+      mbar_arrive(&it_empty[slot]);
       const int4 dsc = __ldg(ca.idesc + gi);
       const int li = dsc.x >> 22, tile = dsc.x & ((1 << 22) - 1);
       const PPArgs& a = ca.L[li];
@@ -869,11 +876,9 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       t.g = dsc.w;
       const int c = row & (a.cout - 1);
       const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
-      // the shortcut rows are written inside this launch: read only once the
-      // accumulator is full (its MMAs ran on stages the producer loaded after
-      // acquiring this tile's dependencies), through L2
-      pp_epi_tile<true>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
-                        true, false);
+      // the shortcut rows are written inside this launch: read through L2 (ld.global.cg)
+      pp_epi_tile<false>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
+                         true, false);
       const unsigned long long e0 = prof ? clock64() : 0;
       if (a.fc_w == nullptr) {  // publish this column half of the tile
         named_bar_sync(2 + ew, 128);
