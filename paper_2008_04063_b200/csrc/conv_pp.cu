@@ -665,7 +665,9 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
   if (warp == 0) {
     if (lane == 0) {
       // -------------------------------------------------------------- producer
-      pdl_wait();
+      // with flagged stems every input of the launch is guarded by a tile counter: no
+      // whole-grid wait on the stem launch (its CTAs are all resident: PDL launched us)
+      if (!ca.stems_flagged) pdl_wait();
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
       const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     const int wq = static_cast<int>(warp) & 3;
     const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
     uint32_t accph = 0;
-    pdl_wait();
+    if (!ca.stems_flagged) pdl_wait();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * 256);
     for (int seq = eb;; seq += 2) {
       const int slot = seq & (kChainRing - 1);
@@ -878,7 +880,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
       // the shortcut rows are written inside this launch: read through L2 (ld.global.cg)
       pp_epi_tile<false>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
-                         true, false);
+                         true, (ca.opts & 4) != 0);
       const unsigned long long e0 = prof ? clock64() : 0;
       if (a.fc_w == nullptr) {  // publish this column half of the tile
         named_bar_sync(2 + ew, 128);
@@ -1087,6 +1089,9 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
     const int R = round_up(8 + nb + dr_max, 8);
     return (2u * 2u * a.Q * R * 16u <= budget) && R / 8 <= 256;
   };
+  // a member's last conv keeps the shape-only tile model: its width sets the fp32 grouping of the
+  // mean-pool partials, and a bed's logit stays bit-identical across the chain / per-layer paths
+  if (fc_w != nullptr) prefer_nb = 0;
   if (prefer_nb > 0) {
     // K4c: narrower tiles for short layers, whose few tiles per bed otherwise
     // leave a persistent CTA waiting on the previous layer's last tiles
@@ -1192,7 +1197,7 @@ void free_chain(ChainPlan* cp) {
 // side by side and a CTA changes weight image only at layer boundaries --
 // and steals from the other queues once its own is drained, which evens out
 // the cost model's error at the end of the launch.
-const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms) {
+const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms, const ChainStemIn* stems) {
   free_chain(cp);
   if (n < 1 || n > kMaxChainLayers) return "chain: layer count out of range";
   cp->args = new ChainArgs();
@@ -1200,12 +1205,23 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
   std::memset(&ca, 0, sizeof(ca));
   std::vector<CUtensorMap> tm(2 * n);
   int n_chains = 0, flags = 0;
-  // HB_CHAIN_OPTS (experiments): 1 = no proxy fence on the consumer side
+  for (int i = 0; i < n; ++i) n_chains = std::max(n_chains, in[i].chain + 1);
+  // the stems' tile counters first (when they publish them), then the layers'
+  std::vector<int> stem_base(n_chains, -1);
+  if (stems)
+    for (int k = 0; k < n_chains; ++k) {
+      stem_base[k] = flags;
+      flags += stems[k].rows * stems[k].tiles_per_row;
+    }
+  // HB_CHAIN_OPTS (experiments): 1 = no proxy fence on the consumer side, 4 = no epilogue math or
+  // stores (timing only: the outputs are garbage)
   ca.opts = getenv("HB_CHAIN_OPTS") ? atoi(getenv("HB_CHAIN_OPTS")) : 0;
   uint32_t smem = 0;
   for (int i = 0; i < n; ++i) {
     const PPPlan& p = *in[i].plan;
     if (in[i].dep_in >= i || in[i].dep_res >= i) return "chain: a layer depends on a later one";
+    if ((in[i].dep_in == kChainDepStem || in[i].dep_res == kChainDepStem) && !stems)
+      return "chain: a stem dependency without stem counters";
     if (p.args.dbg) return "chain: debug knobs (HB_PP_DBG) are per-launch only";
     ca.L[i] = p.args;
     if (ca.L[i].n_stages > kChainStages) ca.L[i].n_stages = kChainStages;
@@ -1223,7 +1239,11 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
   for (int i = 0; i < n; ++i) {  // a dependency must be on the same chain with the same row numbering
     for (int d : {in[i].dep_in, in[i].dep_res})
       if (d >= 0 && (in[d].chain != in[i].chain || ca.L[d].P != ca.L[i].P)) return "chain: bad dependency";
+    if (stems && (in[i].dep_in == kChainDepStem || in[i].dep_res == kChainDepStem) &&
+        stems[in[i].chain].rows != ca.L[i].P)
+      return "chain: stem rows differ from the layer's";
   }
+  ca.stems_flagged = stems != nullptr;
   // One queue per (chain, group member): a member's layers use one weight
   // image each, so a CTA drawing from one queue changes image only at layer
   // boundaries.  CTA blocks per queue in proportion to the MMA work (largest
@@ -1289,6 +1309,7 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
   std::vector<int4> idesc(items.size()), ideps(items.size());
   auto dep_range = [&](int dl, int row, long lo, long hi, int* f0, int* f1) {
     *f0 = *f1 = 0;
+    if (dl < 0) return;  // written before the launch
     const PPArgs& d = ca.L[dl];
     lo = std::max(lo, 0L);
     hi = std::min(hi, static_cast<long>(d.out_rows));
@@ -1308,7 +1329,28 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     idesc[k] = make_int4(items[k], p, nt, g);
     int4 dr = make_int4(0, 0, 0, 0);
     const long r0 = 8L * (nt * (a.nb / 8) - 1);
+    // the stem's tiles: 1024-position blocks x groups_per_blk phase groups per block
+    auto stem_range = [&](int row, long lo, long hi, int* f0, int* f1) {
+      const ChainStemIn& sm = stems[in[i].chain];
+      lo = std::max(lo, 0L);
+      hi = std::min(hi, static_cast<long>(sm.out_rows));
+      *f0 = *f1 = 0;
+      if (hi <= lo) return;
+      const int base = stem_base[in[i].chain] + row * sm.tiles_per_row;
+      *f0 = base + static_cast<int>(lo / 1024) * sm.groups_per_blk;
+      *f1 = std::min(base + static_cast<int>((hi - 1) / 1024 + 1) * sm.groups_per_blk, base + sm.tiles_per_row);
+    };
+    if (ca.dep_in[i] == kChainDepStem) stem_range(p, a.Q * r0, a.Q * (r0 + a.R), &dr.x, &dr.y);
     if (ca.dep_in[i] >= 0) dep_range(ca.dep_in[i], p, a.Q * r0, a.Q * (r0 + a.R), &dr.x, &dr.y);
+    if (ca.dep_res[i] == kChainDepStem) {
+      const long ppt = static_cast<long>(a.ph) * a.nb;
+      if (a.n_res_pairs)
+        stem_range(p, a.ph * r0, a.ph * (r0 + a.R), &dr.z, &dr.w);
+      else if (a.res_mode == 1)
+        stem_range(p, ppt * nt, ppt * (nt + 1), &dr.z, &dr.w);
+      else if (a.res_mode == 2)
+        stem_range(p, 2 * ppt * nt, 2 * ppt * (nt + 1), &dr.z, &dr.w);
+    }
     if (ca.dep_res[i] >= 0) {
       const long ppt = static_cast<long>(a.ph) * a.nb;
       if (a.n_res_pairs)
@@ -1341,6 +1383,8 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
       cudaMalloc(&cp->d_sync, sizeof(unsigned) * (2 + nq)) != cudaSuccess ||
       cudaMemset(cp->d_sync, 0, sizeof(unsigned) * (2 + nq)) != cudaSuccess)
     return "chain: device allocation failed";
+  if (stems)
+    for (int k = 0; k < n_chains; ++k) cp->stem_flags.push_back(cp->d_flags + stem_base[k]);
   ca.tmaps = cp->d_tmaps;
   ca.items = cp->d_items;
   ca.queue_off = cp->d_item_off;

@@ -185,6 +185,7 @@ struct hb_ctx {
   // with tile-level dependencies; each layer writes its own buffer (no reuse
   // inside a tick, so no write-after-read hazard between tiles)
   bool chain_on = false;
+  int stem_sms = 0;  // chain mode: CTAs of the stem launch (0 = one per SM); the chain takes the other SMs first
   ChainPlan chain;
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
@@ -291,14 +292,24 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   // the aggregate (captured as parallel graph branches).  The eager profiling
   // path (pr->ev set) keeps everything on one stream so per-kernel event times
   // stay clean.
-  if (c->chain_on) {  // stems, then every group's conv chain in one launch
-    for (const Group& g : c->groups) {
-      const int G = static_cast<int>(g.mi.size());
-      const double rows = static_cast<double>(c->Pc) * G;
+  if (c->chain_on) {  // every group's stem in one launch, then every group's conv chain in one launch
+    std::vector<StemGroup> sg;
+    for (size_t gi = 0; gi < c->groups.size(); ++gi) {
+      const Group& g = c->groups[gi];
       const LayerSpec& s0 = g.layers[0];
-      CK(c, launch_stem(g.stem[0].data(), G, round_up(c->W, 8), c->Pc, c->W, layer_in_q(g.layers[1], g.kind[1]),
-                        s0.cout, s0.pad, g.cbuf[0], st));
-      pr->mark(st, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+      sg.push_back({g.stem[0].data(), static_cast<int>(g.mi.size()), round_up(c->W, 8), c->Pc, c->W,
+                    layer_in_q(g.layers[1], g.kind[1]), s0.cout, s0.pad, g.cbuf[0],
+                    c->chain.stem_flags.empty() ? nullptr : c->chain.stem_flags[gi]});
+    }
+    if (pr->ev) {  // eager profile: one stem launch per group (per-kernel times)
+      for (size_t gi = 0; gi < sg.size(); ++gi) {
+        const LayerSpec& s0 = c->groups[gi].layers[0];
+        const double rows = static_cast<double>(c->Pc) * c->groups[gi].mi.size();
+        CK(c, launch_stems(&sg[gi], 1, c->stem_sms, st));
+        pr->mark(st, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+      }
+    } else {
+      CK(c, launch_stems(sg.data(), static_cast<int>(sg.size()), c->stem_sms, st));
     }
     CK(c, launch_chain(c->chain, st));
     pr->mark(st, K_CHAIN, c->chain.flops, c->chain.bytes);
@@ -483,7 +494,7 @@ int build_selection(hb_ctx* c) {
     {  // head partials per patient of the last layer, as that layer is tiled
       const LayerSpec& H = g.layers.back();
       if (g.kind.back() == KIND_PP) {
-        g.head_mt = pp_head_mt(H, G, c->Pc, c->num_sms, c->chain_on ? chain_nb() : 0);
+        g.head_mt = pp_head_mt(H, G, c->Pc, c->num_sms);  // (the head's tile width is shape-only in both paths)
         if (g.head_mt <= 0) return fail(c, HB_E_INVALID, "conv_pp: head layer does not plan");
       } else {
         const int bn = conv_bn(H.cout), sm = conv_stride_m(conv_fold(H.cin, H.cout, H.stride));
@@ -564,6 +575,24 @@ int build_selection(hb_ctx* c) {
     }
   }
   if (c->chain_on) {  // the chain's layer list: groups in order, layer-major; dependencies inside a group
+    // HB_CHAIN_STEM_FLAGS=1: the stems publish tile counters (the stem_pp kernel serves every
+    // chain-eligible width) and the chain's first layers start on published stem tiles
+    const char* sf = getenv("HB_CHAIN_STEM_FLAGS");
+    const char* hs = getenv("HB_STEM");
+    // default off: the stem and the first layers share one HBM-bound phase, so overlapping them
+    // measured no gain (tools/abtick.py: 0.626 ms whole-launch wait vs 0.639-0.709 ms with counters,
+    // stem grids of 32-148 CTAs)
+    bool flag_stems = (sf ? atoi(sf) : 0) != 0 && (hs ? atoi(hs) : 1) != 0;
+    std::vector<ChainStemIn> stems;
+    for (const Group& g : c->groups) {
+      const LayerSpec& s0 = g.layers[0];
+      const int oq = layer_in_q(g.layers[1], g.kind[1]);
+      const int tpr = stem_tiles_per_row(c->W, oq, s0.cout);
+      const int blocks = (act_rows_q(c->W, oq) + 1023) / 1024;  // 1024-position blocks per row
+      flag_stems = flag_stems && tpr > 0;
+      stems.push_back({tpr, tpr / blocks, act_rows_q(c->W, oq), c->Pc * static_cast<int>(g.mi.size())});
+    }
+    c->stem_sms = flag_stems ? (getenv("HB_STEM_SMS") ? atoi(getenv("HB_STEM_SMS")) : 0) : 0;
     std::vector<ChainLayerIn> cl;
     double flops = 0, bytes = 0;
     for (size_t gi = 0; gi < c->groups.size(); ++gi) {
@@ -574,8 +603,9 @@ int build_selection(hb_ctx* c) {
         const LayerSpec& L = g.layers[li];
         ChainLayerIn x;
         x.plan = &c->plans[g.plan0[0] + li - 1].pp;
-        x.dep_in = li >= 2 ? first + static_cast<int>(li) - 2 : -1;
-        x.dep_res = (li % 2 == 0 && li >= 3) ? first + static_cast<int>(li) - 3 : -1;
+        x.dep_in = li >= 2 ? first + static_cast<int>(li) - 2 : (flag_stems ? kChainDepStem : -1);
+        x.dep_res = (li % 2 == 0 && li >= 3) ? first + static_cast<int>(li) - 3
+                                             : (li == 2 && flag_stems ? kChainDepStem : -1);
         x.chain = static_cast<int>(gi);
         cl.push_back(x);
         flops += rows * 2.0 * L.cin * L.cout * kTaps * L.lout;
@@ -585,7 +615,8 @@ int build_selection(hb_ctx* c) {
     }
     int grid = c->num_sms;  // HB_CHAIN_SMS caps the persistent grid (tests: many items per CTA, stealing)
     if (const char* cs = getenv("HB_CHAIN_SMS")) grid = std::max(1, std::min(grid, atoi(cs)));
-    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), grid);
+    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), grid,
+                               flag_stems ? stems.data() : nullptr);
     if (e) return fail(c, HB_E_INVALID, e);
     c->chain.flops = flops;
     c->chain.bytes = bytes;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <utility>
+#include <vector>
 
 namespace hb {
 
@@ -149,6 +150,7 @@ struct ChainArgs {
   const int4* ideps;               // per item: counter index ranges [x, y) (input) and [z, w) (shortcut)
   unsigned* flags;                 // tile counters (+2 per launch: two column halves)
   int opts;                        // HB_CHAIN_OPTS experiment bits
+  int stems_flagged;               // the stems publish tile counters: no whole-grid wait on them
   unsigned* sync;                  // [0] finished launches (epoch), [1] CTAs out of the current launch
   unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
   unsigned long long* trace;       // HB_CHAIN_PROF: per queue item [5] globaltimer ns: pulled, weights in place,
@@ -156,8 +158,13 @@ struct ChainArgs {
 };
 struct ChainLayerIn {
   const struct PPPlan* plan;
-  int dep_in, dep_res;
+  int dep_in, dep_res;             // chain layer index, -1 = written before the launch, kChainDepStem = the stem
   int chain;                       // independent sequence (a member group): CTAs are partitioned by chain
+};
+constexpr int kChainDepStem = -2;
+// A chain's stem when it publishes tile counters (launch_stems): its tile grid.
+struct ChainStemIn {
+  int tiles_per_row, groups_per_blk, out_rows, rows;
 };
 struct ChainPlan {
   ChainArgs* args = nullptr;       // host copy of the parameter block
@@ -170,6 +177,7 @@ struct ChainPlan {
   unsigned long long* d_trace = nullptr;
   int4* d_idesc = nullptr;
   int4* d_ideps = nullptr;
+  std::vector<unsigned*> stem_flags;  // per chain: its stem's tile counters (inside d_flags), when flagged
   int n_items = 0;
   int grid = 0, n_layers = 0;
   uint32_t smem_bytes = 0;
@@ -187,7 +195,9 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
                     const float* fc_w = nullptr, float* head_out = nullptr, size_t head_g_stride = 0,
                     int prefer_nb = 0 /* column tile to use where it fits (K4c), 0 = the tile model */);
 cudaError_t launch_pp(const PPPlan& plan, cudaStream_t st);
-const char* plan_chain(ChainPlan* cp, const ChainLayerIn* layers, int n_layers, int num_sms);
+// stems: per chain, or null (every stem output is complete before the launch: PDL wait)
+const char* plan_chain(ChainPlan* cp, const ChainLayerIn* layers, int n_layers, int num_sms,
+                       const ChainStemIn* stems = nullptr);
 void free_chain(ChainPlan* cp);
 cudaError_t launch_chain(const ChainPlan& cp, cudaStream_t st);
 cudaError_t init_pp_kernel();
@@ -247,6 +257,20 @@ struct StemMember {
 constexpr int kMaxGroup = 16;
 cudaError_t launch_stem(const StemMember* members /*host array, G entries*/, int G, int x_stride, int Pm, int L,
                         int out_q, int cout, int pad, __half* out, cudaStream_t st);  // out: Q-phase layout
+// Several member groups' stems in one launch (one programmatic predecessor for
+// the K4c chain), on at most grid_cap CTAs (0 = one per SM).  With `flags` set
+// each tile publishes itself (+1 per column half; tile = row * tiles_per_row +
+// block * groups_per_block + phase group, row = g * Pm + p): the chain's first
+// layers start on published tiles while the stem still runs.
+struct StemGroup {
+  const StemMember* members;  // host array, G entries
+  int G, x_stride, Pm, L, out_q, cout, pad;
+  __half* out;
+  unsigned* flags;            // tile counters or null
+};
+cudaError_t launch_stems(const StemGroup* groups, int n, int grid_cap, cudaStream_t st);
+// Stem tiles per activation row (1024-position blocks x phase groups); 0 = the builder kernel serves the shape
+int stem_tiles_per_row(int L, int out_q, int cout);
 
 // K1+K2: ring append of `n_new` samples per stream at the device write cursor
 // *wpos, then (if xn != null) gather of the window ending at *wpos + n_new and

@@ -31,6 +31,7 @@
 // its B image (fp16 weights) and bias resident in smem, so member changes cost
 // nothing.
 #include <algorithm>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 
@@ -314,6 +315,7 @@ static cudaError_t launch_stem_toeplitz(const StemMember* members, int G, int x_
 // Warp roles as in K4b: 0 TMA, 1 MMA, 2 TMEM, 4-19 four epilogue warpgroups
 // (buffer = ew & 1, half of the tile's (phase pair, 8-channel) units = ew >> 1).
 constexpr int kStemPPThreads = 640;
+constexpr int kStemSubs = 4;
 constexpr int kStemPPStages = 8;
 constexpr int kStemSeg = 2560;  // one tile's window segment: 5 boxes of 256 samples (1048 used)
 
@@ -324,6 +326,16 @@ struct StemPPArgs {
   int J, dd, paired, groups_per_blk, nt_per_row, num_tiles, n_stages;
   int dbg;  // HB_STEM_DBG (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA
   __half* out;
+  unsigned* flags;  // per tile counter (+1 per column half after its stores), null = none (see launch_stems)
+};
+// One launch = up to kStemSubs independent stems (member groups of different
+// widths): CTAs [cta0[i], cta0[i+1]) run sub-problem i with its own smem
+// layout.  A single launch gives the K4c chain ONE programmatic predecessor.
+struct StemPPLaunch {
+  CUtensorMap tm[kStemSubs];
+  StemPPArgs a[kStemSubs];
+  int cta0[kStemSubs + 1];
+  int n_sub;
 };
 
 // (lo, hi) -> max(0, .) rounded to fp16, lo in the low half (one F2FP.RELU)
@@ -343,9 +355,22 @@ __device__ __forceinline__ void st_global_256(void* p, const uint32_t (&v)[8]) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(kStemPPThreads, 1)
-    stem_pp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ StemPPArgs a) {
+// Processing order k -> tile index: the group's members interleaved bed by bed
+// (row = g * Pm + p in memory), so every member's first beds land first -- the
+// K4c chain's per-member queues start on them while the stem still runs.
+__device__ __forceinline__ int stem_tile_of(const StemPPArgs& a, int k) {
+  const int ro = k / a.nt_per_row, rt = k - ro * a.nt_per_row;
+  const int row = (ro % a.G) * a.Pm + ro / a.G;
+  return row * a.nt_per_row + rt;
+}
+
+__global__ void __launch_bounds__(kStemPPThreads, 1) stem_pp_kernel(const __grid_constant__ StemPPLaunch S) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  int sub = 0;
+  while (sub + 1 < S.n_sub && static_cast<int>(blockIdx.x) >= S.cta0[sub + 1]) ++sub;
+  const StemPPArgs& a = S.a[sub];
+  const CUtensorMap* tmX = &S.tm[sub];
+  const int bid = static_cast<int>(blockIdx.x) - S.cta0[sub], nbk = S.cta0[sub + 1] - S.cta0[sub];
   const int wimg = a.Ceff * 32;                                   // one (phase, k-step) B image
   uint8_t* sW = smem;                                             // [G][8 phases][2 k-steps][k-half][Ceff][16 B]
   uint8_t* sX = sW + static_cast<size_t>(a.G) * 16 * wimg;        // [n_stages][kStemSeg]
@@ -415,11 +440,12 @@ __global__ void __launch_bounds__(kStemPPThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA
     if (lane == 0) {
-      prefetch_tmap(&tmX);
+      prefetch_tmap(tmX);
       pdl_wait();  // x is the window kernel's output
       int st = 0;
       uint32_t sph = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      for (int k = bid; k < a.num_tiles; k += nbk) {
+        const int tile = stem_tile_of(a, k);
         const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
         const int nb = rt / a.groups_per_blk;
         const int g = row / a.Pm, p = row - g * a.Pm;
@@ -430,7 +456,7 @@ __global__ void __launch_bounds__(kStemPPThreads, 1)
           mbar_arrive_expect_tx(&st_full[st], static_cast<uint32_t>(kStemSeg));
           uint8_t* dst = sX + st * kStemSeg;
           for (int b = 0; b < kStemSeg / 512; ++b)  // samples [l0 - 8, l0 + 1272), 16-B aligned start
-            tma_load_2d(dst + 512 * b, &tmX, &st_full[st], nb * 1024 - 8 + 256 * b, a.x_row0[g] + p);
+            tma_load_2d(dst + 512 * b, tmX, &st_full[st], nb * 1024 - 8 + 256 * b, a.x_row0[g] + p);
         }
         if (++st == a.n_stages) {
           st = 0;
@@ -443,7 +469,8 @@ __global__ void __launch_bounds__(kStemPPThreads, 1)
     const uint32_t idesc = make_idesc_f16(kBM, a.Ceff);
     int st = 0, acc = 0;
     uint32_t sph = 0, accph = 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+    for (int k = bid; k < a.num_tiles; k += nbk) {
+      const int tile = stem_tile_of(a, k);
       const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
       const int g = row / a.Pm, jg = rt % a.groups_per_blk;
       mbar_wait(&st_full[st], sph, 332);
@@ -488,7 +515,8 @@ __global__ void __launch_bounds__(kStemPPThreads, 1)
     const int u_lo = (ew >> 1) ? (units + 1) / 2 : 0, u_hi = (ew >> 1) ? units : (units + 1) / 2;
     uint32_t accph = 0;
     pdl_wait();  // the output buffer may still be read by the previous tick's layers
-    for (int tile = blockIdx.x + eb * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
+    for (int k = bid + eb * nbk; k < a.num_tiles; k += 2 * nbk) {
+      const int tile = stem_tile_of(a, k);
       const int row = tile / a.nt_per_row, rt = tile - row * a.nt_per_row;
       const int nb = rt / a.groups_per_blk, jg = rt - nb * a.groups_per_blk;
       const int g = row / a.Pm;
@@ -563,6 +591,14 @@ __global__ void __launch_bounds__(kStemPPThreads, 1)
         tc_fence_before();
         mbar_arrive(&acc_empty[eb]);
       }
+      if (a.flags) {  // publish this half of the tile for the K4c chain (counters grow by 2 per tick)
+        named_bar_sync(2 + ew, 128);
+        if (wq == 0 && lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.flags + tile), "r"(1u) : "memory");
+        }
+      }
       accph ^= 1u;
     }
   }
@@ -576,10 +612,18 @@ cudaError_t init_stem_pp_kernel() {
   return cudaFuncSetAttribute(stem_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
 }
 
-cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
-                        __half* out, cudaStream_t st) {
-  const int which = getenv("HB_STEM") ? atoi(getenv("HB_STEM")) : 1;  // read per launch (tests switch it)
-  if (!which) return launch_stem_toeplitz(members, G, x_stride, Pm, L, out_q, cout, pad, out, st);
+// One group's stem as stem_pp sub-problems (several when the members' B
+// images do not fit one CTA's shared memory).  Returns false when stem_pp does
+// not serve the shape (w > 64: the Toeplitz builder kernel).
+struct StemPPSub {
+  CUtensorMap tm;
+  StemPPArgs a;
+  size_t smem;
+};
+static cudaError_t plan_stem_pp(const StemGroup& sg, std::vector<StemPPSub>* subs, bool* served) {
+  const StemMember* members = sg.members;
+  const int G = sg.G, x_stride = sg.x_stride, Pm = sg.Pm, L = sg.L, out_q = sg.out_q, cout = sg.cout, pad = sg.pad;
+  *served = false;
   if (cout > 128 || cout % 8 || G < 1 || G > kMaxGroup || pad < 0 || pad > 8 || (x_stride * 2) % 16 ||
       out_q < 1 || out_q > 32 || (out_q & (out_q - 1)))
     return cudaErrorInvalidValue;
@@ -597,7 +641,8 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
   a.J = 8;  // phases per tile (8, 4 or 2): J * Ceff TMEM columns per accumulator
   while (a.J > 2 && a.J * a.Ceff > 256) a.J >>= 1;
   // two phases per tile (C > 64) leave too little per accumulator: the builder kernel is faster there
-  if (a.J < 4) return launch_stem_toeplitz(members, G, x_stride, Pm, L, out_q, cout, pad, out, st);
+  if (a.J < 4) return cudaSuccess;
+  *served = true;
   a.dd = out_q < a.J ? out_q : 1;  // pair phases j, j + dd
   a.paired = a.dd == out_q;        // ... which are adjacent 16-B rows of the layout
   a.groups_per_blk = 8 / a.J;
@@ -620,9 +665,6 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
       return cudaErrorNotSupported;
     enc = reinterpret_cast<EncodeTiledFnStem>(fp);
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t plane_elems = static_cast<size_t>(a.out_rows) * 8;
   for (int g0 = 0; g0 < G; g0 += gmax) {
     const int Gs = G - g0 < gmax ? G - g0 : gmax;
@@ -637,24 +679,91 @@ cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, 
       a.x_row0[g] = static_cast<int>(off / x_stride);
       rows = a.x_row0[g] + Pm > rows ? a.x_row0[g] + Pm : rows;
     }
-    CUtensorMap tm;
+    StemPPSub sub;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(x_stride) * 2};
     const cuuint32_t box[2] = {256, 1};
     const cuuint32_t estr[2] = {1, 1};
-    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
+    if (enc(&sub.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
     a.G = Gs;
     a.num_tiles = Gs * Pm * a.nt_per_row;
-    a.out = out + static_cast<size_t>(g0) * Pm * (cout / 8) * plane_elems;
-    const int grid = a.num_tiles < sms ? a.num_tiles : sms;
-    const cudaError_t e =
-        launch_pdl(stem_pp_kernel, dim3(grid), dim3(kStemPPThreads), fixed + Gs * per_g, st, tm, a);
+    a.out = sg.out + static_cast<size_t>(g0) * Pm * (cout / 8) * plane_elems;
+    // the counters index the group's tiles (rows g * Pm + p over ALL its members)
+    a.flags = sg.flags ? sg.flags + static_cast<size_t>(g0) * Pm * a.nt_per_row : nullptr;
+    sub.a = a;
+    sub.smem = fixed + Gs * per_g;
+    subs->push_back(sub);
+  }
+  return cudaSuccess;
+}
+
+int stem_tiles_per_row(int L, int out_q, int cout) {
+  const int Ceff = cout < 16 ? 16 : round_up(cout, 16);
+  int J = 8;
+  while (J > 2 && J * Ceff > 256) J >>= 1;
+  if (J < 4) return 0;
+  return ((act_rows_q(L, out_q) + 1023) / 1024) * (8 / J);
+}
+
+cudaError_t launch_stems(const StemGroup* groups, int n, int grid_cap, cudaStream_t st) {
+  const int which = getenv("HB_STEM") ? atoi(getenv("HB_STEM")) : 1;  // read per launch (tests switch it)
+  std::vector<StemPPSub> subs;
+  for (int i = 0; i < n; ++i) {
+    const StemGroup& sg = groups[i];
+    bool served = false;
+    if (which) {
+      const cudaError_t e = plan_stem_pp(sg, &subs, &served);
+      if (e != cudaSuccess) return e;
+    }
+    if (!served) {
+      if (sg.flags) return cudaErrorInvalidValue;  // the builder kernel publishes no tile counters
+      const cudaError_t e = launch_stem_toeplitz(sg.members, sg.G, sg.x_stride, sg.Pm, sg.L, sg.out_q, sg.cout, sg.pad,
+                                                 sg.out, st);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int cap = grid_cap > 0 ? std::min(grid_cap, sms) : sms;
+  for (size_t s0 = 0; s0 < subs.size(); s0 += kStemSubs) {
+    const int ns = static_cast<int>(std::min<size_t>(kStemSubs, subs.size() - s0));
+    StemPPLaunch S;
+    std::memset(&S, 0, sizeof(S));
+    S.n_sub = ns;
+    long tot = 0;
+    size_t smem = 0;
+    for (int i = 0; i < ns; ++i) {
+      S.tm[i] = subs[s0 + i].tm;
+      S.a[i] = subs[s0 + i].a;
+      tot += S.a[i].num_tiles;
+      smem = std::max(smem, subs[s0 + i].smem);
+    }
+    // CTAs per sub-problem in proportion to its tiles (>= 1 each), at most one per tile
+    const int grid = static_cast<int>(std::min<long>(tot, std::max(cap, ns)));
+    int given = 0;
+    S.cta0[0] = 0;
+    for (int i = 0; i < ns; ++i) {
+      int c = i + 1 == ns ? grid - given
+                          : static_cast<int>(std::max<long>(1, static_cast<long>(grid) * S.a[i].num_tiles / tot));
+      c = std::max(1, std::min(c, grid - given - (ns - 1 - i)));
+      c = std::min(c, S.a[i].num_tiles);
+      given += c;
+      S.cta0[i + 1] = given;
+    }
+    const cudaError_t e = launch_pdl(stem_pp_kernel, dim3(given), dim3(kStemPPThreads), smem, st, S);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_stem(const StemMember* members, int G, int x_stride, int Pm, int L, int out_q, int cout, int pad,
+                        __half* out, cudaStream_t st) {
+  StemGroup sg{members, G, x_stride, Pm, L, out_q, cout, pad, out, nullptr};
+  return launch_stems(&sg, 1, 0, st);
 }
 
 }  // namespace hb
