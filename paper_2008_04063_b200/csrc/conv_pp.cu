@@ -1288,15 +1288,32 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     });
     for (size_t r = 0; left > 0; r = (r + 1) % rem.size(), --left) ctas[rem[r].second] += 1;
   }
-  // queue items: layer-major, the member's tiles in (patient, column) order
+  // queue items: the member's tiles in (patient, column) order, layer-major -- except that the
+  // leading run of large layers (HB_CHAIN_CHUNKS > 1) goes bed chunk by bed chunk: all those
+  // layers over the first chunk's beds, then over the next chunk's, so a layer reads its producer
+  // layer's output (and its block input) while they are still in L2.  Every item still follows
+  // all the items it depends on (same beds, earlier layers; rows are per bed).
+  const int n_chunks = getenv("HB_CHAIN_CHUNKS") ? std::max(1, atoi(getenv("HB_CHAIN_CHUNKS"))) : 1;
+  const int chunk_min = getenv("HB_CHAIN_CHUNK_MIN") ? atoi(getenv("HB_CHAIN_CHUNK_MIN")) : 128;
   std::vector<int> items, qoff(nq + 1, 0), home(grid, 0);
   for (int q = 0; q < nq; ++q) {
     qoff[q] = static_cast<int>(items.size());
-    for (int i = 0; i < n; ++i) {
-      if (in[i].chain != q_chain[q]) continue;
-      const int per_g = ca.L[i].Pm * ca.L[i].nt_per_p;
-      for (int t = q_member[q] * per_g; t < (q_member[q] + 1) * per_g; ++t) items.push_back((i << 22) | t);
+    std::vector<int> ls;  // this chain's layers, in order
+    for (int i = 0; i < n; ++i)
+      if (in[i].chain == q_chain[q]) ls.push_back(i);
+    size_t pre = 0;  // the chunked prefix: layers with >= chunk_min tiles per (member, chunk)
+    while (n_chunks > 1 && pre < ls.size() && ca.L[ls[pre]].Pm * ca.L[ls[pre]].nt_per_p / n_chunks >= chunk_min) ++pre;
+    auto emit = [&](int i, int p0, int p1) {
+      const int ntp = ca.L[i].nt_per_p;
+      const int t0 = (q_member[q] * ca.L[i].Pm + p0) * ntp, t1 = (q_member[q] * ca.L[i].Pm + p1) * ntp;
+      for (int t = t0; t < t1; ++t) items.push_back((i << 22) | t);
+    };
+    if (pre > 0) {
+      const int Pm = ca.L[ls[0]].Pm;
+      for (int c = 0; c < n_chunks; ++c)
+        for (size_t k = 0; k < pre; ++k) emit(ls[k], c * Pm / n_chunks, (c + 1) * Pm / n_chunks);
     }
+    for (size_t k = pre; k < ls.size(); ++k) emit(ls[k], 0, ca.L[ls[k]].Pm);
   }
   qoff[nq] = static_cast<int>(items.size());
   {

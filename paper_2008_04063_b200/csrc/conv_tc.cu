@@ -137,8 +137,9 @@ __device__ __forceinline__ void fetch_round(uint32_t taddr, int bn, bool two, in
   }
 }
 
-// MMA issue for one k-chunk with `F` taps folded into N (warp-uniform walk,
-// one elected lane issues; two 64-bit descriptor adds per MMA).
+// MMA issue for one k-chunk with `F` taps folded into N, by the calling
+// (elected) lane: two descriptor adds per MMA, no per-MMA election (the issue
+// loop is on the tensor pipe's critical path, as in K4b).
 template <int F, typename ToffS2>
 __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                              uint32_t idesc, uint32_t& accum, int per_tap, uint32_t rows16,
@@ -149,7 +150,7 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
       uint64_t ad = adesc + static_cast<uint32_t>(2 * j) * rows16 + static_cast<uint32_t>(-a.pad - a.row0);
 #pragma unroll
       for (int q = 0; q < kTaps / F; ++q) {
-        if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+        mma_f16_ss(d_tmem, ad, bd, idesc, accum);
         accum = 1u;
         ad += F;
         bd += btap;
@@ -159,10 +160,10 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
       uint64_t a0 = ag + toff_s2(0), a1 = ag + toff_s2(1);
 #pragma unroll
       for (int q = 0; q < kTaps / (2 * F); ++q) {
-        if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+        mma_f16_ss(d_tmem, a0, bd, idesc, accum);
         accum = 1u;
         bd += btap;
-        if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+        mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
         bd += btap;
         a0 += F;
         a1 += F;
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         // toff(t) rows: s=1 -> t - pad - row0 (+1 per tap); s=2 -> even/odd
         // taps alternate parity regions, each advancing one row per tap pair.
         uint32_t accum = kc > 0 ? 1u : 0u;
+        if (elect_one()) {
         if (per_tap > 0) {
           // K-steps are (tap group q, 16-channel sub-chunk j); a tap group is
           // `fold` taps sharing one A view (s=1: taps qF..qF+F-1; s=2: taps of
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint64_t ad = adesc + static_cast<uint32_t>(-a.pad - a.row0);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-              if (elect_one()) mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+              mma_f16_ss(d_tmem, ad, bd, idesc, accum);
               accum = 1u;
               ad += 2;
               bd += bstep16;
@@ -377,23 +379,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint64_t a0 = adesc + toff_s2(0), a1 = adesc + toff_s2(1);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              if (elect_one()) mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+              mma_f16_ss(d_tmem, a0, bd, idesc, accum);
               accum = 1u;
               bd += bstep16;
-              if (elect_one()) mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+              mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
               bd += bstep16;
               a0 += 2;
               a1 += 2;
             }
           }
         }
-        __syncwarp();
-        if (prof) t_issue += clock64() - t0;
-        if (elect_one()) {
-          mma_commit(&a_empty[as]);
+          mma_commit(&a_empty[as]);  // the same lane that issued the k-chunk's MMAs
           if (!a.b_resident) mma_commit(&b_empty[bs]);
         }
         __syncwarp();
+        if (prof) t_issue += clock64() - t0;
         if (!a.b_resident && ++bs == a.nb_slots) {
           bs = 0;
           bph ^= 1;

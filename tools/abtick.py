@@ -13,6 +13,7 @@ from paper_2008_04063_b200.engine import EnsembleEngine  # noqa: E402
 from paper_2008_04063_b200.zoo import Selector, holmes_zoo  # noqa: E402
 
 P = int(os.environ.get("AB_P", "64"))
+SEL = os.environ.get("AB_SEL", "c2")  # "c2" (the benchmark's 4 members) or "all" (the 60-member zoo, c3)
 zoo = holmes_zoo()
 engs = []
 base = dict(os.environ)
@@ -23,7 +24,8 @@ for cfg in sys.argv[1:]:
         env[k] = v
     os.environ.clear()
     os.environ.update(env)
-    e = EnsembleEngine(zoo, Selector.from_indices(60, [10, 13, 30, 50]), P, hop=250)
+    sel = Selector.ones(60) if SEL == "all" else Selector.from_indices(60, [10, 13, 30, 50])
+    e = EnsembleEngine(zoo, sel, P, hop=250)
     e.ingest(np.random.default_rng(0).standard_normal((P, 3, 7500)).astype(np.float32))
     e.prepare()
     engs.append((cfg, e))
@@ -32,6 +34,6 @@ os.environ.update(base)
 res = {c: [] for c, _ in engs}
 for r in range(int(os.environ.get("AB_ROUNDS", "8"))):
     for c, e in engs:
-        res[c].append(e.time_tick(25) * 1e3)
+        res[c].append(e.time_tick(int(os.environ.get("AB_TICKS", "25"))) * 1e3)
 for c, v in res.items():
     print(f"{c:40s} median {np.median(v):.4f} ms  min {min(v):.4f}  max {max(v):.4f}")
