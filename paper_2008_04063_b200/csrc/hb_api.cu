@@ -4,6 +4,8 @@
 #include "../../include/holmes_b200.h"
 #include "hb_kernels.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named host ranges for nsys / ncu --nvtx
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -17,6 +19,12 @@ using namespace hb;
 namespace {
 
 thread_local std::string g_create_err;
+
+// RAII NVTX range over a C-ABI call (free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct LayerSpec {
   int cin, cout, stride, lin, lout, pad, res_mode, res_c, head;
@@ -364,6 +372,7 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
 
 int build_selection(hb_ctx* c) {
   if (!c->dirty) return HB_OK;
+  NvtxRange nv("hb:build_selection");
   free_selection(c);
   if (c->selected.empty()) return fail(c, HB_E_EMPTY, "cannot serve an empty ensemble");
   const int M = static_cast<int>(c->selected.size());
@@ -852,6 +861,7 @@ int hb_selected(const hb_ctx* c, int* idx_out, int cap) {
 
 int hb_ingest(hb_ctx* c, const float* samples, int n, void* stream) {
   if (!c || (!samples && n > 0)) return fail(c, HB_E_INVALID, "null argument");
+  NvtxRange nv("hb:ingest");
   if (n < 0) return fail(c, HB_E_INVALID, "n_per_stream must be >= 0");
   cudaSetDevice(c->device);
   cudaStream_t st = pick(c, stream);
@@ -904,6 +914,7 @@ int hb_tick_submit(hb_ctx* c, const float* samples, int slot, void* stream) {
 namespace {
 int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool overlap_h2d) {
   if (!c) return fail(c, HB_E_INVALID, "null argument");
+  NvtxRange nv("hb:tick_submit");
   if (slot < 0 || slot > 1) return fail(c, HB_E_INVALID, "slot must be 0 or 1");
   cudaSetDevice(c->device);
   cudaStream_t st = pick(c, stream);
@@ -939,6 +950,7 @@ int tick_submit(hb_ctx* c, const float* samples, int slot, void* stream, bool ov
 
 int hb_tick_collect(hb_ctx* c, int slot, float* member_logits, float* ens_prob, float* ens_mean_logit) {
   if (!c) return fail(c, HB_E_INVALID, "null argument");
+  NvtxRange nv("hb:tick_collect");
   if (slot < 0 || slot > 1) return fail(c, HB_E_INVALID, "slot must be 0 or 1");
   if (!c->io_busy[slot]) return fail(c, HB_E_STATE, "slot " + std::to_string(slot) + " has no submitted tick");
   cudaSetDevice(c->device);
@@ -956,6 +968,7 @@ int hb_tick_collect(hb_ctx* c, int slot, float* member_logits, float* ens_prob, 
 int hb_tick(hb_ctx* c, const float* samples, float* member_logits, float* ens_prob, float* ens_mean_logit,
             void* stream) {
   if (!c) return fail(c, HB_E_INVALID, "null argument");
+  NvtxRange nv("hb:tick");
   const bool host_out = member_logits || ens_prob || ens_mean_logit;
   if (host_out) {
     int slot = c->io_busy[0] ? (c->io_busy[1] ? -1 : 1) : 0;

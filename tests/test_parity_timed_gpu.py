@@ -218,3 +218,37 @@ def test_k4b_planner_variants_match_oracle(tmp_path, env):
     ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, C2), streams, int(got["end"]),
                                        beds=beds)
     _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
+
+
+def test_k4c_timeline_is_complete_and_causal(monkeypatch):
+    """The chain launch's per-item timeline (HB_CHAIN_PROF=1, `hb_chain_trace`): every queue item of
+    every layer was pulled, got its weight image, had its dependencies met and published both column
+    halves, in that order; and within each member chain no layer's item had its dependencies met
+    before the first tile of the layer it reads was published."""
+    import ctypes as C
+
+    from paper_2008_04063_b200 import _lib
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    monkeypatch.setenv("HB_CHAIN", "1")
+    monkeypatch.setenv("HB_CHAIN_PROF", "1")
+    P = 16
+    with EnsembleEngine(holmes_zoo(), Selector.from_indices(60, C2), P, hop=250) as eng:
+        eng.ingest(synth.ecg_block(3, P, 3, 0, W))
+        eng.time_tick(2)
+        cap = 1 << 18
+        tr = np.zeros((cap, 5), np.uint64)
+        items = np.zeros(cap, np.int32)
+        n = _lib.lib().hb_chain_trace(eng._h, tr.ctypes.data_as(C.c_void_p), items.ctypes.data_as(C.c_void_p), cap)
+    assert n > 0
+    tr, items = tr[:n].astype(np.int64), items[:n]
+    assert (tr > 0).all(), "an item was never pulled, readied or published"
+    assert (tr[:, 0] <= tr[:, 1]).all() and (tr[:, 1] <= tr[:, 2]).all()
+    assert (tr[:, 2] <= tr[:, 3]).all() and (tr[:, 2] <= tr[:, 4]).all()
+    layer = items >> 22
+    done = np.maximum(tr[:, 3], tr[:, 4])
+    # chain layers in order: w32 group (16 conv layers), then w64 (8): layer j > first of its group reads j - 1
+    firsts = {0, 16}
+    for j in sorted(set(layer.tolist())):
+        if j in firsts:
+            continue
+        assert tr[layer == j, 2].min() >= done[layer == j - 1].min(), j
