@@ -168,7 +168,7 @@ __device__ __forceinline__ void pp_issue_pair(const PPArgs& a, uint32_t d_tmem, 
 // kLateRes: read the shortcut only after the accumulator wait (K4c: the rows
 // are written inside the same launch); otherwise the first two chunks' rows
 // are requested before it.  Returns after arriving on acc_empty.
-template <bool kLateRes>
+template <bool kLateRes, int kParts>
 __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, int ew, int wq, int lane,
                                             uint32_t taddr, uint64_t* acc_full, uint32_t accph,
                                             uint64_t* acc_empty, float bias, bool cg, bool skip_math) {
@@ -179,8 +179,14 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
   const int phase = ph - 1 - (row >> lc);
   const int g8 = c >> 3;
   const int r8 = lane & 7;
-  const int nch = a.nb >> 4;  // 16-column chunks; this warpgroup takes half (the first the larger)
-  const int c_lo = (ew >> 1) ? (nch + 1) >> 1 : 0, c_hi = (ew >> 1) ? nch : (nch + 1) >> 1;
+  // 16-column chunks; this warpgroup drains part `ew` of kParts (the first parts the larger).  The
+  // fused head writes one partial per QUARTER of the columns whatever kParts is (a part of a half
+  // split covers two quarters), so the fp32 grouping of a bed's head sum is the same in K4b
+  // (quarters) and K4c (halves): both paths stay bit-identical.
+  const int nch = a.nb >> 4;
+  const int c_lo = (ew * nch + kParts - 1) / kParts, c_hi = ((ew + 1) * nch + kParts - 1) / kParts;
+  constexpr int kQ = kHeadParts / kParts;  // head quarters per part
+  const int q0 = ew * kQ;                  // first quarter of this part
   const int step = 8 * ph;
   const int l0 = ph * (t.nt * a.nb + r8) + phase;
   const int h_valid = l0 < a.lout ? (a.lout - l0 + step - 1) / step : 0;
@@ -204,7 +210,8 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
   const float* fcw = a.fc_w;
   __half* outp = fcw ? nullptr : a.out + q_off(static_cast<size_t>(t.p) * (cout >> 3) + g8, a.out_qs, a.out_lq, l0);
   const int o_inc = (step >> a.out_qs) * 8;
-  float head = 0.f;
+  float head0 = 0.f, head1 = 0.f;  // quarter q0 (and q0 + 1 when a part spans two quarters)
+  const int q_split = ((q0 + 1) * nch + kHeadParts - 1) / kHeadParts;  // first chunk of quarter q0 + 1
   float fc8[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) fc8[q] = fcw ? __ldg(fcw + static_cast<size_t>(t.g) * cout + g8 * 8 + q) : 0.f;
@@ -253,7 +260,7 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
     }
     if (res_mode && ch + 2 < c_hi) load_res(ch + 2, raw);
     tmem_wait_ld();
-    if (ch == c_hi - 1) {  // this warpgroup's columns drained
+    if (ch == c_hi - 1) {  // this warpgroup's columns drained (a part is never empty: nb >= 64)
       tc_fence_before();
       mbar_arrive(acc_empty);
     }
@@ -289,7 +296,10 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float2 f = __half22float2(o2[q]);
-            head = fmaf(f.x, fc8[2 * q], fmaf(f.y, fc8[2 * q + 1], head));
+            if (kQ > 1 && ch >= q_split)
+              head1 = fmaf(f.x, fc8[2 * q], fmaf(f.y, fc8[2 * q + 1], head1));
+            else
+              head0 = fmaf(f.x, fc8[2 * q], fmaf(f.y, fc8[2 * q + 1], head0));
           }
         }
       }
@@ -301,10 +311,15 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
   }
   if (fcw != nullptr) {  // one partial per (tile, epilogue warp), summed in fixed order by K5
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) head += __shfl_xor_sync(0xffffffffu, head, off);
-    if (lane == 0)
-      a.head_out[static_cast<size_t>(t.g) * a.head_g_stride + static_cast<size_t>(t.p - t.g * a.Pm) * a.head_mt +
-                 static_cast<size_t>(t.nt) * 8 + (ew >> 1) * 4 + wq] = head;  // (column half, warp)
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) {
+      float hv = i == 0 ? head0 : head1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
+      if (lane == 0)
+        a.head_out[static_cast<size_t>(t.g) * a.head_g_stride + static_cast<size_t>(t.p - t.g * a.Pm) * a.head_mt +
+                   static_cast<size_t>(t.nt) * (4 * kHeadParts) + (q0 + i) * 4 + wq] = hv;  // (column quarter, warp)
+    }
   }
 }
 
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     mbar_init(w_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 256);  // two epilogue warpgroups per buffer
+      mbar_init(&acc_empty[i], 128 * kEpiPartsPP);  // every epilogue warpgroup drains its part of every tile
     }
     fence_barrier_init();
     // the first weight image (immutable, so before the dependency wait) goes out
@@ -480,13 +495,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
-    // Four warpgroups: ew & 1 = accumulator buffer (every other tile), ew >> 1
-    // = which half of the tile's columns.  The accumulator is held while its
-    // columns are drained, so the MMA of tile k+2 waits for the epilogue of
-    // tile k: two warpgroups per buffer halve that hold time (measured: with
-    // one warpgroup per buffer the MMA warp spent most of its time waiting).
+    // Four warpgroups, each drains one quarter of every tile's columns (part
+    // ew).  The accumulator is held while its columns are drained and the MMA
+    // of tile k+2 waits for the epilogue of tile k: splitting each tile over
+    // all four warpgroups (instead of two per buffer, alternate tiles) halves
+    // that hold time; the total epilogue work is the same.
     const int ew = (static_cast<int>(warp) - 4) >> 2;
-    const int eb = ew & 1;
     const int wq = static_cast<int>(warp) & 3;
     const int c = (wq * 32 + static_cast<int>(lane)) & (a.cout - 1);
     for (int i = static_cast<int>(threadIdx.x) - 128; i < a.G * a.cout; i += kPPThreads - 128) {
@@ -494,15 +508,15 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       s_bias[i] = a.bias[static_cast<size_t>(g) * a.bias_stride + (i - g * a.cout)];
     }
     named_bar_sync(1, kPPThreads - 128);  // the epilogue warps alone: off the producer's path
-    uint32_t accph = 0;
     pdl_wait();
     const CtaRange cr = cta_range(a);
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
-    for (int tile = cr.first + eb * cr.stride; tile < cr.end; tile += 2 * cr.stride) {
+    int k = 0;
+    for (int tile = cr.first; tile < cr.end; tile += cr.stride, ++k) {
       const PPTile t = pp_tile(a, tile);
-      pp_epi_tile<false>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb],
-                         s_bias[t.g * a.cout + c], (a.dbg & 64) != 0, (a.dbg & 1) != 0);
-      accph ^= 1u;
+      const int eb = k & 1;  // the accumulator the MMA used for this tile
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * a.nb);
+      pp_epi_tile<false, kEpiPartsPP>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], static_cast<uint32_t>(k >> 1) & 1u,
+                         &acc_empty[eb], s_bias[t.g * a.cout + c], (a.dbg & 64) != 0, (a.dbg & 1) != 0);
     }
   }
 
@@ -645,11 +659,11 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     mbar_init(w_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 256);
+      mbar_init(&acc_empty[i], 128 * kEpiPartsChain);  // the two warpgroups of that accumulator
     }
     for (int i = 0; i < kChainRing; ++i) {
       mbar_init(&it_full[i], 1);
-      mbar_init(&it_empty[i], 1 + 256);  // the MMA warp + the two epilogue warpgroups of that parity
+      mbar_init(&it_empty[i], 1 + 128 * kEpiPartsChain);  // the MMA warp + the two epilogue warpgroups of that parity
       mbar_init(&it_ready[i], 1);
     }
     fence_barrier_init();
@@ -670,7 +684,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       if (!ca.stems_flagged) pdl_wait();
       const bool prof = ca.prof != nullptr;
       unsigned long long p_dep = 0, p_w = 0, p_st = 0, p_start = prof ? clock64() : 0;
-      const uint32_t target = 2u * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
+      // counters grow by kEpiPartsChain per launch for a chain layer's tile (one per epilogue part), by 2
+      // for a stem tile (two column halves)
+      const uint32_t epoch1 = *reinterpret_cast<volatile unsigned*>(ca.sync) + 1u;
+      const uint32_t target = static_cast<uint32_t>(kEpiPartsChain) * epoch1, target_stem = 2u * epoch1;
       int cur_key = first >= 0 ? item_key(first) : -1, reloads = 0;
       int st = 0;
       uint32_t empty_ph = 0;  // per stage slot: parity of its uses so far
@@ -717,7 +734,14 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
         const int line0 = t.nt * (a.nb / 8) - 1;  // rows from n0 - 8
         {  // counters of the producer tiles this item's TMA boxes read (ranges decoded on the host)
           const int4 dr = __ldg(ca.ideps + gi);
-          chain_wait_ranges(ca.flags, dr.x, dr.y, dr.z, dr.w, target);
+          const uint32_t t_in = ca.dep_in[li] == kChainDepStem ? target_stem : target;
+          const uint32_t t_res = ca.dep_res[li] == kChainDepStem ? target_stem : target;
+          if (t_in == t_res) {
+            chain_wait_ranges(ca.flags, dr.x, dr.y, dr.z, dr.w, t_in);
+          } else {
+            chain_wait_ranges(ca.flags, dr.x, dr.y, 0, 0, t_in);
+            chain_wait_ranges(ca.flags, dr.z, dr.w, 0, 0, t_res);
+          }
         }
         if (trace) trace[5 * gi + 2] = globaltimer();
         if (!(ca.opts & 1)) fence_proxy_async_global();
@@ -853,13 +877,14 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     const int ew = (static_cast<int>(warp) - 4) >> 2;
     const bool prof = ca.prof != nullptr && warp == 4 && lane == 0;
     unsigned long long e_work = 0, e_start = prof ? clock64() : 0;
-    const int eb = ew & 1;
+    const int eb = ew & 1;     // this warpgroup's accumulator: items of that parity
+    const int half = ew >> 1;  // ... and its half of their columns
     const int wq = static_cast<int>(warp) & 3;
     const int row = wq * 32 + static_cast<int>(lane);  // M row = (p', c)
-    uint32_t accph = 0;
     if (!ca.stems_flagged) pdl_wait();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(eb * 256);
     for (int seq = eb;; seq += 2) {
+      const uint32_t accph = static_cast<uint32_t>(seq >> 1) & 1u;
       const int slot = seq & (kChainRing - 1);
       mbar_wait(&it_full[slot], static_cast<uint32_t>(seq / kChainRing) & 1u, 219);
       const int gi = ring[slot];
@@ -879,10 +904,10 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       const int c = row & (a.cout - 1);
       const float bias = __ldg(a.bias + static_cast<size_t>(t.g) * a.bias_stride + c);
       // the shortcut rows are written inside this launch: read through L2 (ld.global.cg)
-      pp_epi_tile<false>(a, t, ew, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph, &acc_empty[eb], bias,
-                         true, (ca.opts & 4) != 0);
+      pp_epi_tile<false, kEpiPartsChain>(a, t, half, wq, static_cast<int>(lane), taddr, &acc_full[eb], accph,
+                                         &acc_empty[eb], bias, true, (ca.opts & 4) != 0);
       const unsigned long long e0 = prof ? clock64() : 0;
-      if (a.fc_w == nullptr) {  // publish this column half of the tile
+      if (a.fc_w == nullptr) {  // publish this column half of the tile (+1 of kEpiPartsChain per launch)
         named_bar_sync(2 + ew, 128);
         if (wq == 0 && lane == 0) {
           fence_proxy_async_global();
@@ -890,9 +915,8 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
         }
       }
-      if (ca.trace && wq == 0 && lane == 0) ca.trace[5 * gi + 3 + (ew >> 1)] = globaltimer();
+      if (ca.trace && wq == 0 && lane == 0) ca.trace[5 * gi + 3 + half] = globaltimer();
       if (prof) e_work += clock64() - e0;
-      accph ^= 1u;
     }
     if (prof) {
       unsigned long long* pr = ca.prof + blockIdx.x * 16;
@@ -1120,7 +1144,7 @@ const char* plan_pp(PPPlan* plan, int G, int Pm, int cin, int cout, int lin, int
   a.out = out;
   a.fc_w = fc_w;
   a.head_out = head_out;
-  a.head_mt = a.nt_per_p * 8;
+  a.head_mt = a.nt_per_p * 4 * kHeadParts;  // one partial per (column tile, column quarter, warp)
   a.head_g_stride = head_g_stride ? head_g_stride : static_cast<size_t>(Pm) * a.head_mt;
   a.res = res;
   a.res_mode = (res && !res_mma) ? res_mode : 0;  // the epilogue's share of the shortcut

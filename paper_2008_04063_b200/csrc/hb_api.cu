@@ -68,7 +68,7 @@ bool pp_eligible(const LayerSpec& L) {
   static const bool heads = !(getenv("HB_PP_HEAD") && atoi(getenv("HB_PP_HEAD")) == 0);
   return (heads || !L.head) && L.cin >= 16 && pp_shape_ok(L.cin, L.cout, L.stride);
 }
-// Head partials per patient of a K4b head layer (nt_per_p * 8), from a dry-run plan.
+// Head partials per patient of a K4b head layer (nt_per_p * 4 * kEpiParts), from a dry-run plan.
 int pp_head_mt(const LayerSpec& L, int G, int Pm, int sms, int prefer_nb = 0) {
   PPPlan plan;
   __half* fake = reinterpret_cast<__half*>(static_cast<uintptr_t>(1) << 20);  // encoded, never dereferenced

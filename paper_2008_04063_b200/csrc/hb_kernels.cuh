@@ -16,6 +16,14 @@ namespace hb {
 
 constexpr int kTaps = 16;
 constexpr int kBM = 128;               // output positions per tile (UMMA M)
+// Epilogue split of a K4b / K4c tile's columns: K4b drains every tile with all
+// four epilogue warpgroups (a quarter each: the accumulator is held half as
+// long), K4c with the two warpgroups of its accumulator's parity (a half each,
+// alternate tiles).  The fused head writes one partial per column QUARTER in
+// both, so a bed's head sum has the same fp32 grouping on either path.
+constexpr int kEpiPartsPP = 4;
+constexpr int kEpiPartsChain = 2;
+constexpr int kHeadParts = 4;
 constexpr int kConvThreads = 384;      // warp0 TMA, warp1 MMA, warp2 TMEM, warps 4-7 / 8-11 epilogue
 constexpr uint32_t kSmemLimit = 232448;  // 227 KB opt-in dynamic smem on sm_100
 
