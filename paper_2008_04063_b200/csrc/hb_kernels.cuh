@@ -142,7 +142,7 @@ struct PPPlan {
 constexpr int kChainStages = 8;          // stage barriers (a layer uses its plan's n_stages <= this)
 constexpr uint32_t kChainFixed = 1024;   // barriers, item ring, TMEM holder, before the weight image
 constexpr int kChainRing = 8;            // items in flight between the producer and the MMA / epilogue roles
-constexpr int kMaxChainLayers = 36;
+constexpr int kMaxChainLayers = 64;  // (the parameter block stays under 17 KB of the 32 KB limit)
 struct ChainArgs {
   PPArgs L[kMaxChainLayers];
   int dep_in[kMaxChainLayers];     // chain layer writing this layer's input (-1: written before the launch)
