@@ -309,15 +309,17 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
                     layer_in_q(g.layers[1], g.kind[1]), s0.cout, s0.pad, g.cbuf[0],
                     c->chain.stem_flags.empty() ? nullptr : c->chain.stem_flags[gi]});
     }
-    if (pr->ev) {  // eager profile: one stem launch per group (per-kernel times)
-      for (size_t gi = 0; gi < sg.size(); ++gi) {
-        const LayerSpec& s0 = c->groups[gi].layers[0];
-        const double rows = static_cast<double>(c->Pc) * c->groups[gi].mi.size();
-        CK(c, launch_stems(&sg[gi], 1, c->stem_sms, st));
-        pr->mark(st, K_STEM, rows * 2.0 * s0.cout * kTaps * s0.lout, rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout));
+    // one launch for every group's stem, in the graph and in the eager profile alike
+    CK(c, launch_stems(sg.data(), static_cast<int>(sg.size()), c->stem_sms, st));
+    {
+      double fl = 0, by = 0;
+      for (const Group& g : c->groups) {
+        const LayerSpec& s0 = g.layers[0];
+        const double rows = static_cast<double>(c->Pc) * g.mi.size();
+        fl += rows * 2.0 * s0.cout * kTaps * s0.lout;
+        by += rows * (2.0 * s0.lin + 2.0 * s0.cout * s0.lout);
       }
-    } else {
-      CK(c, launch_stems(sg.data(), static_cast<int>(sg.size()), c->stem_sms, st));
+      pr->mark(st, K_STEM, fl, by);
     }
     CK(c, launch_chain(c->chain, st));
     pr->mark(st, K_CHAIN, c->chain.flops, c->chain.bytes);
