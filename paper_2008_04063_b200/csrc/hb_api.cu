@@ -425,11 +425,18 @@ int build_selection(hb_ctx* c) {
   for (auto& g : c->groups)
     for (size_t li = 1; li < g.layers.size(); ++li) g.kind[li] = layer_kind(g.layers[li]);
   {  // K4c chain mode: every conv of every group on K4b, one patient chunk, each layer its own buffer
-    // HB_CHAIN=0 keeps the per-layer launches (read per build, so tests can switch it); the
-    // per-launch debug knobs (HB_PP_DBG) exist only there
+    // HB_CHAIN=1 / 0 forces the chain / the per-layer launches (read per build, so tests can
+    // switch it); unset, the chain serves bed counts where it measured faster: 8-128 beds
+    // (tools/abtick.py, c2: 16 beds 0.243 vs 0.272 ms, 64 beds 0.632 vs 0.693, 128 beds even;
+    // 4 beds 0.205 vs 0.156 and 192+ beds slower -- too few tiles per layer to fill a
+    // persistent grid, or enough that per-layer launches amortise their fixed costs).
+    // The per-launch debug knobs (HB_PP_DBG) exist only on the per-layer path.
     const char* ce = getenv("HB_CHAIN");
     const char* dbg = getenv("HB_PP_DBG");
-    bool ok = (ce ? atoi(ce) : 1) != 0 && !(dbg && atoi(dbg));
+    const int chain_mode = ce ? atoi(ce) : -1;
+    const int min_p = getenv("HB_CHAIN_MIN_P") ? atoi(getenv("HB_CHAIN_MIN_P")) : 8;
+    const int max_p = getenv("HB_CHAIN_MAX_P") ? atoi(getenv("HB_CHAIN_MAX_P")) : 128;
+    bool ok = chain_mode != 0 && !(dbg && atoi(dbg)) && (chain_mode > 0 || (c->P >= min_p && c->P <= max_p));
     double bytes = 0;
     int n_layers = 0;
     for (auto& g : c->groups)

@@ -104,9 +104,13 @@ def test_c2_64_beds_every_bed_three_ticks():
     _run(Selector.from_indices(60, C2), 64, 250, 3, 0, list(range(64)), zero_bed=17)
 
 
-def test_north_star_1024_beds_sampled():
+@pytest.mark.parametrize("chain", ["auto", "1"])
+def test_north_star_1024_beds_sampled(monkeypatch, chain):
     """The north-star scale: 1024 beds; 64 beds spread over the range (first, last, and
-    the chunk/tile boundaries in between) against the oracle, 2 ticks."""
+    the chunk/tile boundaries in between) against the oracle, 2 ticks -- on the default path
+    (per-layer launches at this bed count) and with the K4c chain forced."""
+    if chain != "auto":
+        monkeypatch.setenv("HB_CHAIN", chain)
     beds = sorted(set(np.linspace(0, 1023, 62).astype(int).tolist()) | {511, 512})
     _run(Selector.from_indices(60, C2), 1024, 250, 2, 1, beds, zero_bed=511, check_every_tick=False)
 
