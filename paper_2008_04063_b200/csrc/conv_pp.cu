@@ -253,7 +253,7 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
         const __half2* h1 = reinterpret_cast<const __half2*>(&raw[2 * b + 1]);
         __half2* o2 = reinterpret_cast<__half2*>(&rv[b]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) o2[q] = __hmax2(h0[q], h1[q]);
+        for (int q = 0; q < 4; ++q) o2[q] = __hmax2_nan(h0[q], h1[q]);
       } else {
         rv[b] = res_mode ? raw[2 * b] : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -287,7 +287,7 @@ __device__ __forceinline__ void pp_epi_tile(const PPArgs& a, const PPTile& t, in
         __half2* o2 = reinterpret_cast<__half2*>(&pk);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const __half2 y = __hmax2(__hadd2(*reinterpret_cast<const __half2*>(&hv[q]), rr[q]), zero);
+          const __half2 y = __hmax2_nan(__hadd2(*reinterpret_cast<const __half2*>(&hv[q]), rr[q]), zero);
           o2[q] = valid ? y : zero;
         }
         if (outp != nullptr) {

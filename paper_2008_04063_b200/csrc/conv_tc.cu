@@ -54,7 +54,7 @@ __device__ __forceinline__ uint4 res_row(const ConvArgs& a, size_t plane, int l)
   const __half2* h1 = reinterpret_cast<const __half2*>(&r1);
   __half2* o2 = reinterpret_cast<__half2*>(&o);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) o2[k] = __hmax2(h0[k], h1[k]);
+  for (int k = 0; k < 4; ++k) o2[k] = __hmax2_nan(h0[k], h1[k]);
   return o;
 }
 
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
           if (a.relu) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) y[k] = fmaxf(y[k], 0.f);
+            for (int k = 0; k < 8; ++k) y[k] = fmax_nan(y[k], 0.f);
           }
           if (a.fc_w != nullptr) {
             if (valid) {

@@ -249,6 +249,15 @@ __device__ __forceinline__ void transpose8_h2(uint32_t (&h)[4], int r8) {
   }
 }
 
+// ReLU / max-pool that propagate NaN (max.NaN): a non-finite sample in a window
+// then reaches that bed's scores as NaN, as in the fp32 oracle, instead of being
+// clamped to a finite activation by IEEE maxNum.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(kStemThreads, 1)
           __half2* o2 = reinterpret_cast<__half2*>(&pk);
 #pragma unroll
           for (int k = 0; k < 8; k += 2) {
-            const float y0 = fmaxf(v[8 * h + k] + bias[g8 * 8 + k], 0.f);
-            const float y1 = fmaxf(v[8 * h + k + 1] + bias[g8 * 8 + k + 1], 0.f);
+            const float y0 = fmax_nan(v[8 * h + k] + bias[g8 * 8 + k], 0.f);
+            const float y1 = fmax_nan(v[8 * h + k + 1] + bias[g8 * 8 + k + 1], 0.f);
             o2[k / 2] = valid ? __floats2half2_rn(y0, y1) : __floats2half2_rn(0.f, 0.f);
           }
           *reinterpret_cast<uint4*>(a.out + q_off(static_cast<size_t>(row) * (a.cout / 8) + g8, a.out_qs,

@@ -236,3 +236,35 @@ def test_selector_change_refused_while_a_tick_is_uncollected():
         res = eng.tick(np.ascontiguousarray(streams[:, :, W:W + hop]))
         assert res.member_logits.shape == (P, 3)
         _compare(res, *_oracle_tick(zoo, sel_b, streams, W + hop))
+
+
+@pytest.mark.parametrize("chain", ["0", "1"])
+def test_nonfinite_samples_stay_in_their_bed(monkeypatch, chain):
+    """Fault isolation: a NaN sample (bed 3, lead I) and an Inf sample (bed 8, lead III) make
+    exactly the members reading those leads non-finite for those beds -- z-normalisation, the
+    convs (NaN-propagating ReLU / max-pool, as the fp32 oracle), the head and the aggregate are
+    per bed and per lead -- and so the beds' ensemble scores; every other bed, and those beds'
+    other members, are bit-identical to a run on clean streams, on both tick paths."""
+    from paper_2008_04063_b200.engine import EnsembleEngine
+    monkeypatch.setenv("HB_CHAIN", chain)
+    zoo = holmes_zoo()
+    sel = Selector.from_indices(60, C2)
+    P, W, hop = 12, 7500, 250
+    clean = _streams(P, W + hop, seed=21)
+    dirty = clean.copy()
+    dirty[3, 0, W - 40] = np.nan      # bed 3, lead I (read by two members)
+    dirty[8, 2, W + 10] = np.inf      # bed 8, lead III, in the newest hop
+    outs = []
+    for s in (clean, dirty):
+        with EnsembleEngine(zoo, sel, P, hop=hop) as eng:
+            eng.ingest(s[:, :, :W - hop])
+            eng.tick(s[:, :, W - hop:W])
+            outs.append(eng.tick(s[:, :, W:W + hop]))
+    ok = [p for p in range(P) if p not in (3, 8)]
+    assert np.array_equal(outs[0].member_logits[ok], outs[1].member_logits[ok])
+    assert np.array_equal(outs[0].ens_prob[ok], outs[1].ens_prob[ok])
+    assert np.isfinite(outs[0].member_logits).all() and np.isfinite(outs[0].ens_prob).all()
+    ml = outs[1].member_logits    # columns: ecg-i-w32-d8, ecg-i-w64-d4 (lead I), ecg-ii-w32-d8, ecg-iii-w32-d8
+    assert np.isnan(ml[3, :2]).all() and np.array_equal(ml[3, 2:], outs[0].member_logits[3, 2:])
+    assert np.isnan(ml[8, 3]) and np.array_equal(ml[8, :3], outs[0].member_logits[8, :3])
+    assert np.isnan(outs[1].ens_prob[[3, 8]]).all() and np.isnan(outs[1].ens_mean_logit[[3, 8]]).all()
