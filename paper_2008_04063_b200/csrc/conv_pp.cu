@@ -1313,11 +1313,13 @@ const char* plan_chain(ChainPlan* cp, const ChainLayerIn* in, int n, int num_sms
     for (size_t r = 0; left > 0; r = (r + 1) % rem.size(), --left) ctas[rem[r].second] += 1;
   }
   // queue items: the member's tiles in (patient, column) order, layer-major -- except that the
-  // leading run of large layers (HB_CHAIN_CHUNKS > 1) goes bed chunk by bed chunk: all those
+  // leading run of large layers (HB_CHAIN_CHUNKS chunks, default 2) goes bed chunk by bed chunk: all those
   // layers over the first chunk's beds, then over the next chunk's, so a layer reads its producer
   // layer's output (and its block input) while they are still in L2.  Every item still follows
   // all the items it depends on (same beds, earlier layers; rows are per bed).
-  const int n_chunks = getenv("HB_CHAIN_CHUNKS") ? std::max(1, atoi(getenv("HB_CHAIN_CHUNKS"))) : 1;
+  // default 2: the chain's DRAM reads drop from 1.36 to 1.01 GB per c2 tick (ncu) -- neutral on
+  // a cool clock, +1.5-2 % over 1000 power-capped ticks (profiles/r02_ab_chain.txt)
+  const int n_chunks = getenv("HB_CHAIN_CHUNKS") ? std::max(1, atoi(getenv("HB_CHAIN_CHUNKS"))) : 2;
   const int chunk_min = getenv("HB_CHAIN_CHUNK_MIN") ? atoi(getenv("HB_CHAIN_CHUNK_MIN")) : 128;
   std::vector<int> items, qoff(nq + 1, 0), home(grid, 0);
   for (int q = 0; q < nq; ++q) {
