@@ -32,3 +32,7 @@ print(f"eager total {tot:.2f} ms; graph tick {eng.time_tick(3) * 1e3:.2f} ms")
 order = np.argsort(-ms)[:15]
 for i in order:
     print(f"  #{i:4d} {KIND[int(k[i])]:5s} {ms[i] * 1e3:8.1f} us {fl[i] / ms[i] / 1e9 if ms[i] > 0 else 0:7.1f} TF/s {fl[i] / 1e9:8.2f} GFLOP")
+order = np.argsort(-ms)[:25]
+print("top launches: index kind ms TF/s GFLOP MB")
+for i in order:
+    print(f"{i:5d} {KIND[int(k[i])]:6s} {ms[i]:7.3f} {fl[i] / max(ms[i], 1e-9) / 1e9:7.1f} {fl[i] / 1e9:8.1f} {by[i] / 1e6:8.1f}")
