@@ -20,5 +20,8 @@ head -30 gpurun_out/r02_ncu_chain_summary.txt
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_parity_timed_gpu.py -x -q -p no:cacheprovider -k "c2_64 or chain_capped_grid" 2>&1 | tail -3
 timeout 900 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_parity_timed_gpu.py -x -q -p no:cacheprovider -k "chain_capped_grid and 13" 2>&1 | tail -3
 timeout 900 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_parity_timed_gpu.py -x -q -p no:cacheprovider -k "chain_capped_grid and 13" 2>&1 | tail -3
+# the per-layer path (K4b with the all-warpgroup epilogue, K4, stems)
+timeout 900 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_parity_timed_gpu.py -x -q -p no:cacheprovider -k "multi_tile_paths_forced and 6" 2>&1 | tail -3
+timeout 900 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_engine_gpu.py -x -q -p no:cacheprovider -k "sliding or nonfinite" 2>&1 | tail -3
 } > gpurun_out/r02_sanitizer.txt 2>&1
 cat gpurun_out/r02_sanitizer.txt
