@@ -764,7 +764,15 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   const uint32_t b_all = a.b_chunk_bytes * a.n_kchunks;
   a.b_resident = resident;
   a.nb_slots = resident ? a.n_kchunks : 2;
-  const uint32_t b_smem = resident ? b_all : 2 * a.b_chunk_bytes;
+  if (!resident) {
+    // Streamed weights (the wide layers): a k-chunk's B image (up to 64 KB) is
+    // consumed in ~1k MMA cycles, less than one image takes to arrive from L2,
+    // so every extra slot that fits next to 3 A stages is another image in
+    // flight (HB_K4_BSLOTS caps it; 2 = the old double buffer).
+    const int cap = getenv("HB_K4_BSLOTS") ? atoi(getenv("HB_K4_BSLOTS")) : 4;
+    while (a.nb_slots < cap && (a.nb_slots + 1) * a.b_chunk_bytes + 3 * a.a_stage_bytes <= budget) ++a.nb_slots;
+  }
+  const uint32_t b_smem = resident ? b_all : a.nb_slots * a.b_chunk_bytes;
   a.na_stages = static_cast<int>((budget - b_smem) / a.a_stage_bytes);
   const int dbg = getenv("HB_DEBUG") ? atoi(getenv("HB_DEBUG")) : 0;
   const int max_stages = (dbg & 2) ? 8 : (dbg & 4) ? 12 : 4;

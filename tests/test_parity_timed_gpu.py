@@ -257,3 +257,29 @@ def test_k4c_timeline_is_complete_and_causal(monkeypatch):
         if j in firsts:
             continue
         assert tr[layer == j, 2].min() >= done[layer == j - 1].min(), j
+
+
+WIDE = [15, 16, 17, 36]   # w64-d16 (up to 512 channels), w128-d2 (x2, grouped), w128-d4: K4 with streamed weights
+
+
+def test_k4_streamed_weight_slots_bit_identical(tmp_path):
+    """K4's streamed-weight ring depth (HB_K4_BSLOTS: 2 = double buffer, default up to 4 images in
+    flight) changes only when weight images arrive, never the MMA order: the ticks are bit-identical
+    across depths, and both match the oracle."""
+    P, hop, ticks, seed = 4, 250, 1, 11
+    outs = {}
+    for slots in ("2", "3", "4"):
+        out = tmp_path / f"tick{slots}.npz"
+        e = dict(os.environ, HB_K4_BSLOTS=slots)
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, WIDE))], check=True, env=e, timeout=600)
+        outs[slots] = np.load(out)
+    for slots in ("3", "4"):
+        for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+            assert np.array_equal(outs[slots][k], outs["2"][k]), (slots, k)
+    got = outs["4"]
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = list(range(P))
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, WIDE), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
