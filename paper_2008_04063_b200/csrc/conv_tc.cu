@@ -27,6 +27,7 @@
 #include "hb_kernels.cuh"
 #include "hb_ptx.cuh"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -62,14 +63,32 @@ __device__ __forceinline__ uint4 res_row(const ConvArgs& a, size_t plane, int l)
 struct TileIdx {
   int g, nt, p, mt;  // p = global row of the [G*Pm] activation tensors
 };
-__device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile) {
-  const int per_nt = a.Pm * a.mt_per_p;
+// Pair mode: `tile` counts PAIRS of M tiles that share a weight image (member
+// g, N tile nt): the flattened (patient, M tile) index f = 2*pair + rank, so a
+// pair may span two beds (a layer with one M tile per bed still fills both
+// CTAs).  An odd count leaves the last pair's second tile a phantom: M tile
+// mt_per_p of the member's last bed, whose rows are all past the layer.
+template <bool kPair = false>
+__device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile, int rank = 0) {
+  const int per_nt = kPair ? a.mtp_per_p : a.Pm * a.mt_per_p;
   const int per_g = a.n_ntiles * per_nt;
   TileIdx t;
   t.g = tile / per_g;
   int rem = tile - t.g * per_g;
   t.nt = rem / per_nt;
   rem -= t.nt * per_nt;
+  if (kPair) {
+    const int f = 2 * rem + rank;
+    if (f < a.Pm * a.mt_per_p) {
+      const int pl = f / a.mt_per_p;
+      t.mt = f - pl * a.mt_per_p;
+      t.p = t.g * a.Pm + pl;
+    } else {
+      t.mt = a.mt_per_p;
+      t.p = t.g * a.Pm + a.Pm - 1;
+    }
+    return t;
+  }
   const int pl = rem / a.mt_per_p;
   t.mt = rem - pl * a.mt_per_p;
   t.p = t.g * a.Pm + pl;
@@ -82,18 +101,27 @@ __device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile) {
 // lane 0 through a small shared-memory exchange (one named barrier per round).
 constexpr int kXchRound = 3 * 32;            // [warp 0..2][32 channels]
 constexpr int kXchPerWg = 2 * kXchRound;     // double-buffered by round parity
-template <int F>
+// Release of the accumulator after the last TMEM load: a local arrive, or in
+// pair mode an arrive on the leader CTA's barrier (`release_cl`, shared::cluster).
+template <bool kPair>
+__device__ __forceinline__ void acc_release(uint64_t* release, uint32_t release_cl) {
+  tc_fence_before();
+  if constexpr (kPair) {
+    mbar_arrive_cluster(release_cl);
+  } else {
+    mbar_arrive(release);
+  }
+}
+
+template <int F, bool kPair>
 __device__ __forceinline__ void fetch_round(uint32_t taddr, int bn, bool two, int wq, uint32_t lane, float* xch,
-                                            int eg, float* v, uint64_t* release) {
+                                            int eg, float* v, uint64_t* release, uint32_t release_cl) {
   uint32_t r0[16], r1[16];
   tmem_ld16_nw(taddr, r0);
   if (two) tmem_ld16_nw(taddr + 16, r1);
   if constexpr (F == 1) {
     tmem_wait_ld();
-    if (release) {
-      tc_fence_before();
-      mbar_arrive(release);
-    }
+    if (release) acc_release<kPair>(release, release_cl);
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r0[k]);
     if (two) {
@@ -105,10 +133,7 @@ __device__ __forceinline__ void fetch_round(uint32_t taddr, int bn, bool two, in
     tmem_ld16_nw(taddr + static_cast<uint32_t>(bn), s0);
     if (two) tmem_ld16_nw(taddr + static_cast<uint32_t>(bn) + 16, s1);
     tmem_wait_ld();
-    if (release) {
-      tc_fence_before();
-      mbar_arrive(release);
-    }
+    if (release) acc_release<kPair>(release, release_cl);
     if (wq > 0 && lane == 0) {  // my row 0, folded block 1 -> the warp above
       float* d = xch + (wq - 1) * 32;
 #pragma unroll
@@ -140,7 +165,24 @@ __device__ __forceinline__ void fetch_round(uint32_t taddr, int bn, bool two, in
 // MMA issue for one k-chunk with `F` taps folded into N, by the calling
 // (elected) lane: two descriptor adds per MMA, no per-MMA election (the issue
 // loop is on the tensor pipe's critical path, as in K4b).
-template <int F, typename ToffS2>
+template <bool kPair>
+__device__ __forceinline__ void mma_any(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (kPair) {
+    mma_f16_ss_pair(d, ad, bd, idesc, acc);
+  } else {
+    mma_f16_ss(d, ad, bd, idesc, acc);
+  }
+}
+template <bool kPair>
+__device__ __forceinline__ void commit_any(uint64_t* bar) {
+  if constexpr (kPair) {
+    mma_commit_pair(bar);
+  } else {
+    mma_commit(bar);
+  }
+}
+
+template <int F, bool kPair, typename ToffS2>
 __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                              uint32_t idesc, uint32_t& accum, int per_tap, uint32_t rows16,
                                              uint32_t bstep16, uint32_t btap, ToffS2 toff_s2) {
@@ -150,7 +192,7 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
       uint64_t ad = adesc + static_cast<uint32_t>(2 * j) * rows16 + static_cast<uint32_t>(-a.pad - a.row0);
 #pragma unroll
       for (int q = 0; q < kTaps / F; ++q) {
-        mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+        mma_any<kPair>(d_tmem, ad, bd, idesc, accum);
         accum = 1u;
         ad += F;
         bd += btap;
@@ -160,10 +202,10 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
       uint64_t a0 = ag + toff_s2(0), a1 = ag + toff_s2(1);
 #pragma unroll
       for (int q = 0; q < kTaps / (2 * F); ++q) {
-        mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+        mma_any<kPair>(d_tmem, a0, bd, idesc, accum);
         accum = 1u;
         bd += btap;
-        mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+        mma_any<kPair>(d_tmem, a1, bd, idesc, 1u);
         bd += btap;
         a0 += F;
         a1 += F;
@@ -172,12 +214,13 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
   }
 }
 
-template <int F>
+template <int F, bool kPair>
 __global__ void __launch_bounds__(kConvThreads, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ ConvArgs a) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ ConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sB = smem;
-  uint8_t* sA = smem + a.nb_slots * a.b_chunk_bytes;
+  uint8_t* sA = smem + a.nb_slots * a.b_slot_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sA + a.na_stages * a.a_stage_bytes);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + a.na_stages;
@@ -193,9 +236,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  // Pair mode: cluster of two CTAs; rank 0 (the leader) issues every MMA and
+  // owns the full / acc_empty barriers both CTAs' TMA bytes and epilogues count on.
+  const int rank = kPair ? static_cast<int>(cluster_rank()) : 0;
+  const bool leader = rank == 0;
+  const int t_first = kPair ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int t_step = kPair ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
+    if (kPair) prefetch_tmap(&tmB);
     for (int i = 0; i < a.na_stages; ++i) {
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
@@ -206,12 +256,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);  // one epilogue warpgroup per buffer
+      mbar_init(&acc_empty[i], kPair ? 256 : 128);  // one epilogue warpgroup per buffer (per CTA of the pair)
     }
     fence_barrier_init();
     // Weights are immutable: the first tile's resident B goes out right behind
     // the barrier init (before the dependency wait), hiding the prologue.
-    if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {
+    if (!kPair && a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {
       const TileIdx t0 = decode_tile(a, blockIdx.x);
       for (int kc = 0; kc < a.n_kchunks; ++kc) {
         mbar_arrive_expect_tx(&b_full[kc], a.b_chunk_bytes);
@@ -222,10 +272,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   }
-  if (warp == 2) tmem_alloc(tmem_holder, a.tmem_cols);
+  if (warp == 2) {
+    if (kPair) {
+      tmem_alloc_pair(tmem_holder, a.tmem_cols);
+    } else {
+      tmem_alloc(tmem_holder, a.tmem_cols);
+    }
+  }
   const bool smem_bias = a.sb_len > 0;  // every member's bias / fc cached in smem (filled by the epilogue warps)
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync_all();  // the peer's TMA / arrives target the leader's barriers: both initialised first
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   // Programmatic dependent launch: let the next layer's CTAs start their
@@ -248,15 +305,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         return a.wpack + static_cast<size_t>(t.g) * a.wpack_stride +
                (static_cast<size_t>(t.nt) * a.n_kchunks + kc) * a.b_chunk_bytes;
       };
-      if (a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {  // loaded in the prologue
+      if (!kPair && a.b_resident && static_cast<int>(blockIdx.x) < a.num_tiles) {  // loaded in the prologue
         const TileIdx t0 = decode_tile(a, blockIdx.x);
         loaded_key = t0.g * a.n_ntiles + t0.nt;
       }
+      // pair mode: the leader's full barriers (shared::cluster addresses) and the B box shape
+      const int b_rows = static_cast<int>(a.b_slot_bytes >> 7);
+      const int b_box = b_rows < 256 ? b_rows : 256;
       pdl_wait();
       int li = 0;       // local tile count
       int reloads = 0;  // resident-B reloads so far
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++li) {
-        const TileIdx t = decode_tile(a, tile);
+      for (int tile = t_first; tile < a.num_tiles; tile += t_step, ++li) {
+        const TileIdx t = decode_tile<kPair>(a, tile, rank);
         const int p = t.p;
         const int blk = (t.mt * a.stride_m + a.row0) / 8;  // first 128-B line (8 rows)
         const int key = t.g * a.n_ntiles + t.nt;
@@ -271,22 +331,47 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           if (load_b) {
             const int slot = a.b_resident ? kc : bs;
             if (!a.b_resident) mbar_wait(&b_empty[bs], bph ^ 1, 2);
-            mbar_arrive_expect_tx(&b_full[slot], a.b_chunk_bytes);
-            bulk_load(sB + static_cast<size_t>(slot) * a.b_chunk_bytes, b_src(t, kc), a.b_chunk_bytes,
-                      &b_full[slot]);
+            if constexpr (kPair) {
+              // this CTA's half of the k-chunk's image (N rows [rank*bn/2, (rank+1)*bn/2)),
+              // counted on the leader's b_full
+              if (leader) mbar_arrive_expect_tx(&b_full[slot], 2 * a.b_slot_bytes);
+              const uint32_t bar = map_to_rank(&b_full[slot], 0);
+              const size_t off = static_cast<size_t>(t.g) * a.wpack_stride +
+                                 (static_cast<size_t>(t.nt) * a.n_kchunks + kc) * a.b_chunk_bytes +
+                                 static_cast<size_t>(rank) * a.b_slot_bytes;
+              const int row = static_cast<int>(off >> 7);
+              for (int r0 = 0; r0 < b_rows; r0 += b_box)
+                tma_load_2d_pair(sB + static_cast<size_t>(slot) * a.b_slot_bytes + static_cast<size_t>(r0) * 128,
+                                 &tmB, bar, 0, row + r0);
+            } else {
+              mbar_arrive_expect_tx(&b_full[slot], a.b_chunk_bytes);
+              bulk_load(sB + static_cast<size_t>(slot) * a.b_chunk_bytes, b_src(t, kc), a.b_chunk_bytes,
+                        &b_full[slot]);
+            }
             if (!a.b_resident && ++bs == a.nb_slots) {
               bs = 0;
               bph ^= 1;
             }
           }
           mbar_wait(&a_empty[as], aph ^ 1, 3);
-          mbar_arrive_expect_tx(&a_full[as], a.a_stage_bytes);
           uint8_t* dst = sA + static_cast<size_t>(as) * a.a_stage_bytes;
-          if (a.stride == 1) {
-            tma_load_4d(dst, &tmA, &a_full[as], 0, blk, kc * groups, p);
+          if constexpr (kPair) {
+            if (leader) mbar_arrive_expect_tx(&a_full[as], 2 * a.a_stage_bytes);
+            const uint32_t bar = map_to_rank(&a_full[as], 0);
+            if (a.stride == 1) {
+              tma_load_4d_pair(dst, &tmA, bar, 0, blk, kc * groups, p);
+            } else {
+              tma_load_5d_pair(dst, &tmA, bar, 0, blk, 0, kc * groups, p);
+              tma_load_5d_pair(dst + region_bytes, &tmA, bar, 0, blk, 1, kc * groups, p);
+            }
           } else {
-            tma_load_5d(dst, &tmA, &a_full[as], 0, blk, 0, kc * groups, p);
-            tma_load_5d(dst + region_bytes, &tmA, &a_full[as], 0, blk, 1, kc * groups, p);
+            mbar_arrive_expect_tx(&a_full[as], a.a_stage_bytes);
+            if (a.stride == 1) {
+              tma_load_4d(dst, &tmA, &a_full[as], 0, blk, kc * groups, p);
+            } else {
+              tma_load_5d(dst, &tmA, &a_full[as], 0, blk, 0, kc * groups, p);
+              tma_load_5d(dst + region_bytes, &tmA, &a_full[as], 0, blk, 1, kc * groups, p);
+            }
           }
           if (++as == a.na_stages) {
             as = 0;
@@ -294,17 +379,38 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
       }
+      if constexpr (kPair) {
+        // The leader's commits arrive on BOTH CTAs' empty barriers: wait until every
+        // stage / slot this CTA filled has been released before the CTA may exit.
+        if (li > 0) {
+          for (int i = 0; i < a.na_stages; ++i) {
+            mbar_wait(&a_empty[as], aph ^ 1, 4);
+            if (++as == a.na_stages) {
+              as = 0;
+              aph ^= 1;
+            }
+          }
+          for (int i = 0; i < a.nb_slots; ++i) {
+            mbar_wait(&b_empty[bs], bph ^ 1, 5);
+            if (++bs == a.nb_slots) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+        }
+      }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // -------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop with warp-uniform values (kept in uniform
     // registers); one elected lane issues each tcgen05.mma / commit.
-    const uint32_t idesc = make_idesc_f16(kBM, a.bnp);
+    const uint32_t idesc = make_idesc_f16(kPair ? 2 * kBM : kBM, a.bnp);
     const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
-    const uint32_t b_lbo = static_cast<uint32_t>(a.bnp * 16);
+    const int b_n = kPair ? a.bnp / 2 : a.bnp;  // B rows held by this CTA
+    const uint32_t b_lbo = static_cast<uint32_t>(b_n * 16);
     const uint32_t rows16 = static_cast<uint32_t>(a.rows);  // one group column, 16 B units
     const uint32_t region16 = region_bytes >> 4;           // one parity region
-    const uint32_t bstep16 = static_cast<uint32_t>(2 * a.bnp);
+    const uint32_t bstep16 = static_cast<uint32_t>(2 * b_n);
     const int per_tap = a.ck >> 4;  // 0 for 8-channel chunks
     // stride-2 A offset (16 B units) of tap t in {0, 1}: parity region + pair row
     auto toff_s2 = [&](int t) -> uint32_t {
@@ -326,7 +432,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     int kbound = (mkey + 1) * per_key;
     unsigned long long t_acc = 0, t_a = 0, t_issue = 0, t0 = 0;
     const bool prof = (a.dbg & 8) && a.prof;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+    for (int tile = t_first; tile < a.num_tiles; tile += t_step) {
       if (multi_key && tile >= kbound) {
         bres_ph ^= 1;
         mkey = tile / per_key;
@@ -349,7 +455,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         tc_fence_after();
         const uint64_t adesc = make_desc(smem_u32(sA + static_cast<size_t>(as) * a.a_stage_bytes), a_lbo, 128);
-        const uint64_t bdesc = make_desc(smem_u32(sB + static_cast<size_t>(slot) * a.b_chunk_bytes), b_lbo, 128);
+        const uint64_t bdesc = make_desc(smem_u32(sB + static_cast<size_t>(slot) * a.b_slot_bytes), b_lbo, 128);
         // Descriptor walk with two 64-bit adds per MMA.  B K-steps are ordered
         // (tap, 16-channel sub-chunk j); A for tap t is the region shifted by
         // toff(t) rows: s=1 -> t - pad - row0 (+1 per tap); s=2 -> even/odd
@@ -361,7 +467,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // `fold` taps sharing one A view (s=1: taps qF..qF+F-1; s=2: taps of
           // one parity, t0, t0+2, ..), their weights side by side in N.
           const uint32_t btap = static_cast<uint32_t>(per_tap) * bstep16;
-          issue_groups<F>(a, d_tmem, adesc, bdesc, idesc, accum, per_tap, rows16, bstep16, btap, toff_s2);
+          issue_groups<F, kPair>(a, d_tmem, adesc, bdesc, idesc, accum, per_tap, rows16, bstep16, btap, toff_s2);
         } else {
           // 8-channel chunk: one K-step pairs taps (t, t+1) [s=1] or (t, t+2) [s=2],
           // i.e. the same region one row apart (LBO = 16 B)
@@ -370,7 +476,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint64_t ad = adesc + static_cast<uint32_t>(-a.pad - a.row0);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-              mma_f16_ss(d_tmem, ad, bd, idesc, accum);
+              mma_any<kPair>(d_tmem, ad, bd, idesc, accum);
               accum = 1u;
               ad += 2;
               bd += bstep16;
@@ -379,18 +485,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             uint64_t a0 = adesc + toff_s2(0), a1 = adesc + toff_s2(1);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              mma_f16_ss(d_tmem, a0, bd, idesc, accum);
+              mma_any<kPair>(d_tmem, a0, bd, idesc, accum);
               accum = 1u;
               bd += bstep16;
-              mma_f16_ss(d_tmem, a1, bd, idesc, 1u);
+              mma_any<kPair>(d_tmem, a1, bd, idesc, 1u);
               bd += bstep16;
               a0 += 2;
               a1 += 2;
             }
           }
         }
-          mma_commit(&a_empty[as]);  // the same lane that issued the k-chunk's MMAs
-          if (!a.b_resident) mma_commit(&b_empty[bs]);
+          commit_any<kPair>(&a_empty[as]);  // the same lane that issued the k-chunk's MMAs
+          if (!a.b_resident) commit_any<kPair>(&b_empty[bs]);
         }
         __syncwarp();
         if (prof) t_issue += clock64() - t0;
@@ -403,7 +509,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           aph ^= 1;
         }
       }
-      if (elect_one()) mma_commit(&acc_full[acc]);
+      if (elect_one()) commit_any<kPair>(&acc_full[acc]);
       __syncwarp();
       if (multi_key && tile + static_cast<int>(gridDim.x) >= kbound &&
           tile + static_cast<int>(gridDim.x) < a.num_tiles) {  // the next tile needs other weights
@@ -440,9 +546,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       named_bar_sync(3, blockDim.x - 128);  // the epilogue warps alone (ids 1, 2: per-warpgroup exchange)
     }
+    const uint32_t release_cl = kPair ? map_to_rank(&acc_empty[acc], 0) : 0u;
     pdl_wait();
-    for (int tile = blockIdx.x + eg * gridDim.x; tile < a.num_tiles; tile += 2 * gridDim.x) {
-      const TileIdx ti = decode_tile(a, tile);
+    for (int tile = t_first + eg * t_step; tile < a.num_tiles; tile += 2 * t_step) {
+      const TileIdx ti = decode_tile<kPair>(a, tile, rank);
       const int nt = ti.nt;
       const int p = ti.p;
       const int mt = ti.mt;
@@ -489,9 +596,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (q >= nrounds) break;
         const bool two = ng > 4 * q + 2;  // second 16-channel chunk in this round
         float v[32];
-        fetch_round<F>(taddr + static_cast<uint32_t>(q * 32), a.bn, two, wq, lane,
-                       s_xch + eg * kXchPerWg + (xround++ & 1) * kXchRound, eg, v,
-                       q == nrounds - 1 ? &acc_empty[acc] : nullptr);
+        fetch_round<F, kPair>(taddr + static_cast<uint32_t>(q * 32), a.bn, two, wq, lane,
+                              s_xch + eg * kXchPerWg + (xround++ & 1) * kXchRound, eg, v,
+                              q == nrounds - 1 ? &acc_empty[acc] : nullptr, release_cl);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int j = 4 * q + h;
@@ -542,7 +649,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         float* sh = s_head + 4 * eg;
         if (lane == 0) sh[wq] = head;
         named_bar_sync(1 + eg, 128);
-        if (wq == 0 && lane == 0) {
+        if (wq == 0 && lane == 0 && (!kPair || mt < a.mt_per_p)) {  // (pair mode: an odd last tile has no slot)
           const float sum = ((sh[0] + sh[1]) + sh[2]) + sh[3];
           a.head_out[static_cast<size_t>(ti.g) * a.head_g_stride +
                      (static_cast<size_t>(p - ti.g * a.Pm) * a.n_ntiles + nt) * a.mt_per_p + mt] = sum;
@@ -559,8 +666,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync_all();  // the peer's last releases reached the leader; every MMA has completed
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, a.tmem_cols);
+  if (warp == 2) {
+    if (kPair) {
+      tmem_dealloc_pair(tmem_base, a.tmem_cols);
+    } else {
+      tmem_dealloc(tmem_base, a.tmem_cols);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -603,6 +717,24 @@ int conv_fold(int cin, int cout, int stride) {
 }
 
 static int a_rows(int stride) { return stride == 1 ? kRowsS1 : kRowsS2; }
+
+// CTA pairs (cta_group::2) for the streamed-weight layers: two CTAs of a TPC
+// share each MMA (M = 256 = two adjacent M tiles, B split along N), so each
+// SM reads half the weight image per MMA from shared memory and fetches half
+// of it from L2.  Read once per process: the weight packer and the planner
+// must agree.  HB_K4_PAIR=0 keeps single-CTA tiles.
+bool conv_pair(int cin, int cout, int stride) {
+  static const int on = getenv("HB_K4_PAIR") ? atoi(getenv("HB_K4_PAIR")) : 1;
+  if (!on) return false;
+  int resident;
+  const int ck = pick_ck(cin, cout, stride, &resident);
+  if (ck == 0 || resident || conv_fold(cin, cout, stride) != 1) return false;
+  const int bn = conv_bn(cout);
+  if (bn < 128 || bn % 32) return false;
+  const int ksteps = ck >= 16 ? ck : 8;
+  const int half_rows = ksteps * bn / 8;  // 128-B rows of one CTA's half of a k-chunk image
+  return half_rows <= 256 || half_rows % 256 == 0;
+}
 
 // Channels per k-chunk.  Prefer the largest chunk whose whole-layer weights
 // stay resident in smem next to two A stages; otherwise the largest chunk that
@@ -655,9 +787,14 @@ void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) 
   const int nkc = cin / ck;
   const int F = conv_fold(cin, cout, stride);
   const int ksteps = (ck >= 16) ? ck / F : 8;  // K-steps per k-chunk
+  // pair mode: each k-chunk image is two halves, one per CTA of the pair, each
+  // holding N rows [r*bn/2, (r+1)*bn/2) in the same (kstep, half) order
+  const int nr = conv_pair(cin, cout, stride) ? 2 : 1;
+  const int rows = bn / nr;
   size_t o = 0;
   for (int nt = 0; nt < nnt; ++nt)
     for (int kc = 0; kc < nkc; ++kc)
+      for (int rk = 0; rk < nr; ++rk)
       for (int ks = 0; ks < ksteps; ++ks)
         for (int half = 0; half < 2; ++half)
           for (int jj = 0; jj < F; ++jj) {  // N rows: folded tap jj, then output channel
@@ -673,7 +810,7 @@ void pack_weights(const float* w, int cin, int cout, int stride, uint16_t* dst) 
               t = t0 + half * stride;
               c0 = kc * ck;
             }
-            for (int n = 0; n < bn; ++n)
+            for (int n = rk * rows; n < (rk + 1) * rows; ++n)
               for (int j = 0; j < 8; ++j) {
                 const int co = nt * bn + n;
                 const float v = (co < cout) ? w[(static_cast<size_t>(co) * cin + (c0 + j)) * kTaps + t] : 0.f;
@@ -763,16 +900,20 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   const uint32_t budget = kSmemLimit - fixed;
   const uint32_t b_all = a.b_chunk_bytes * a.n_kchunks;
   a.b_resident = resident;
+  a.pair = conv_pair(cin, cout, stride) ? 1 : 0;
+  a.b_slot_bytes = a.pair ? a.b_chunk_bytes / 2 : a.b_chunk_bytes;
+  a.mtp_per_p = (Pm * a.mt_per_p + 1) / 2;               // pairs per (member, N tile)
+  if (a.pair) a.num_tiles = G * a.n_ntiles * a.mtp_per_p;  // M-tile pairs
   a.nb_slots = resident ? a.n_kchunks : 2;
   if (!resident) {
     // Streamed weights (the wide layers): a k-chunk's B image (up to 64 KB) is
     // consumed in ~1k MMA cycles, less than one image takes to arrive from L2,
     // so every extra slot that fits next to 3 A stages is another image in
     // flight (HB_K4_BSLOTS caps it; 2 = the old double buffer).
-    const int cap = getenv("HB_K4_BSLOTS") ? atoi(getenv("HB_K4_BSLOTS")) : 4;
-    while (a.nb_slots < cap && (a.nb_slots + 1) * a.b_chunk_bytes + 3 * a.a_stage_bytes <= budget) ++a.nb_slots;
+    const int cap = getenv("HB_K4_BSLOTS") ? atoi(getenv("HB_K4_BSLOTS")) : (a.pair ? 8 : 4);
+    while (a.nb_slots < cap && (a.nb_slots + 1) * a.b_slot_bytes + 3 * a.a_stage_bytes <= budget) ++a.nb_slots;
   }
-  const uint32_t b_smem = resident ? b_all : a.nb_slots * a.b_chunk_bytes;
+  const uint32_t b_smem = resident ? b_all : a.nb_slots * a.b_slot_bytes;
   a.na_stages = static_cast<int>((budget - b_smem) / a.a_stage_bytes);
   const int dbg = getenv("HB_DEBUG") ? atoi(getenv("HB_DEBUG")) : 0;
   const int max_stages = (dbg & 2) ? 8 : (dbg & 4) ? 12 : 4;
@@ -798,8 +939,9 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.head_out = head_out;
   a.head_g_stride = head_g_stride ? head_g_stride : static_cast<size_t>(Pm) * a.n_ntiles * a.mt_per_p;
   a.dbg = dbg;
-  plan->smem_bytes = a.nb_slots * a.b_chunk_bytes + a.na_stages * a.a_stage_bytes + fixed;
+  plan->smem_bytes = a.nb_slots * a.b_slot_bytes + a.na_stages * a.a_stage_bytes + fixed;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
+  if (a.pair) plan->grid = 2 * std::min(a.num_tiles, num_sms / 2);  // clusters of two CTAs
 
   EncodeTiledFn enc = get_encode();
   if (!enc) return "conv: cuTensorMapEncodeTiled unavailable";
@@ -824,13 +966,27 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (rc != CUDA_SUCCESS) return "conv: cuTensorMapEncodeTiled rejected the activation view";
+  if (a.pair) {  // the group's packed weights as 128-B rows; one box = up to 256 rows of one CTA's half
+    const cuuint64_t rows = static_cast<cuuint64_t>(G) * a.wpack_stride / 128;
+    const int b_rows = static_cast<int>(a.b_slot_bytes / 128);
+    const cuuint64_t dims[2] = {64, rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(b_rows < 256 ? b_rows : 256)};
+    rc = enc(&plan->tmapB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint8_t*>(wpack), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) return "conv: cuTensorMapEncodeTiled rejected the weight view";
+  }
   return nullptr;
 }
 
 cudaError_t init_conv_kernel() {
-  cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  cudaError_t e =
+      cudaFuncSetAttribute(conv_tc_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(conv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    e = cudaFuncSetAttribute(conv_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(conv_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
   return e;
 }
 
@@ -840,13 +996,25 @@ cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st) {
   cfg.blockDim = dim3(kConvThreads);
   cfg.dynamicSmemBytes = plan.smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (plan.args.pair) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  if (plan.args.fold == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<2>, plan.tmap, plan.args);
-  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1>, plan.tmap, plan.args);
+  cfg.numAttrs = na;
+  if (plan.args.pair) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1, true>, plan.tmap, plan.tmapB, plan.args);
+  if (plan.args.fold == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<2, false>, plan.tmap, plan.tmapB, plan.args);
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1, false>, plan.tmap, plan.tmapB, plan.args);
 }
 
 }  // namespace hb

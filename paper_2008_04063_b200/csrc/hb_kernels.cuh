@@ -86,11 +86,15 @@ struct ConvArgs {
   size_t head_g_stride;            // floats between members' head partials (patient-chunked groups)
   int dbg;                         // experiments only (HB_DEBUG env)
   unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]
+  int pair;                        // CTA pairs (cta_group::2, M = 256 = two M tiles, B split along N)
+  int mtp_per_p;                   // pair mode: M-tile pairs per (member, N tile) (num_tiles counts pairs)
+  uint32_t b_slot_bytes;           // B bytes per slot in this CTA (pair mode: half a k-chunk's image)
 };
 
 struct ConvPlan {
   ConvArgs args;
   CUtensorMap tmap;                // A operand view of the input activation
+  CUtensorMap tmapB;               // pair mode: the packed weight images as 128-B rows
   int grid;
   uint32_t smem_bytes;
 };

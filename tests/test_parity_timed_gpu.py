@@ -283,3 +283,27 @@ def test_k4_streamed_weight_slots_bit_identical(tmp_path):
     ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, WIDE), streams, int(got["end"]),
                                        beds=beds)
     _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
+
+
+def test_k4_cta_pairs_bit_identical(tmp_path):
+    """K4 on CTA pairs (HB_K4_PAIR=1: cta_group::2, M = 256 over two CTAs, weights split along N
+    and streamed through the leader's barriers) against single-CTA tiles: each output element sees
+    the same MMA sequence, so the ticks are bit-identical; both match the oracle.  Odd tile counts
+    (the last pair's second tile past the layer) and the head layers' partials are covered by the
+    w64-d16 member's short deep layers."""
+    P, hop, ticks, seed = 5, 250, 1, 12
+    outs = {}
+    for pair in ("0", "1"):
+        out = tmp_path / f"tick{pair}.npz"
+        e = dict(os.environ, HB_K4_PAIR=pair)
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, WIDE))], check=True, env=e, timeout=600)
+        outs[pair] = np.load(out)
+    for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+        assert np.array_equal(outs["1"][k], outs["0"][k]), k
+    got = outs["1"]
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = list(range(P))
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, WIDE), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
