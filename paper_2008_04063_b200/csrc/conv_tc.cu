@@ -99,6 +99,13 @@ __device__ __forceinline__ TileIdx decode_tile(const ConvArgs& a, int tile, int 
 // so out[r, c] = D'[r, (0, c)] + D'[r + 1, (1, c)] for F = 2.  Row r + 1 of the
 // same warp comes by shuffle; lane 31 takes row 32(w+1) from the next warp's
 // lane 0 through a small shared-memory exchange (one named barrier per round).
+#ifndef HB_K4_RES_PREFETCH
+#define HB_K4_RES_PREFETCH 8
+#endif
+// Shortcut groups fetched before the accumulator wait.  16 lifts the 128-channel
+// shortcut layers 15 % alone (zero data) but spills and leaves the power-capped
+// c3 tick unchanged (47.4 vs 47.4 ms, profiles/r02_k4_wide_slots.txt): 8 stays.
+constexpr int kResPrefetch = HB_K4_RES_PREFETCH;
 constexpr int kXchRound = 3 * 32;            // [warp 0..2][32 channels]
 constexpr int kXchPerWg = 2 * kXchRound;     // double-buffered by round parity
 // Release of the accumulator after the last TMEM load: a local arrive, or in
@@ -563,9 +570,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       // groups while the MMAs of this tile are still running.
       // identity: block input in I layout; maxpool: block input in S layout,
       // max(x[2l], x[2l+1]) = max(even plane row l, odd plane row l).
-      uint4 rres[8];
+      uint4 rres[kResPrefetch];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kResPrefetch; ++j) {
         rres[j] = make_uint4(0u, 0u, 0u, 0u);
         const int g = g0 + j;
         if (j < ng && g < res_groups && valid) {
@@ -609,8 +616,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int k = 0; k < 8; ++k) y[k] = v[8 * h + k] + bias_t[8 * j + k];
           if (g < res_groups && valid) {
             uint4 rv;
-            if (j < 8) {
-              rv = rres[j < 8 ? j : 0];
+            if (j < kResPrefetch) {
+              rv = rres[j < kResPrefetch ? j : 0];
             } else {
               rv = res_row(a, static_cast<size_t>(p) * res_groups + g, l);
             }
