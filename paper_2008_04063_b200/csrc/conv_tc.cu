@@ -948,7 +948,7 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.dbg = dbg;
   plan->smem_bytes = a.nb_slots * a.b_slot_bytes + a.na_stages * a.a_stage_bytes + fixed;
   plan->grid = a.num_tiles < num_sms ? a.num_tiles : num_sms;
-  if (a.pair) plan->grid = 2 * std::min(a.num_tiles, num_sms / 2);  // clusters of two CTAs
+  if (a.pair) plan->grid = 2 * std::max(1, std::min(a.num_tiles, num_sms / 2));  // clusters of two CTAs
 
   EncodeTiledFn enc = get_encode();
   if (!enc) return "conv: cuTensorMapEncodeTiled unavailable";
