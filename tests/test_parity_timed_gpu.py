@@ -307,3 +307,18 @@ def test_k4_cta_pairs_bit_identical(tmp_path):
     ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, WIDE), streams, int(got["end"]),
                                        beds=beds)
     _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
+
+
+def test_k4_cta_pairs_under_lane_caps(tmp_path):
+    """CTA-pair K4 launches inside SM-capped lanes (HB_LANE_SMS=1,2,3,5: a lane below two SMs still
+    gets one cluster; odd caps round down to whole pairs): bit-identical to the uncapped tick."""
+    P, hop, ticks, seed = 3, 250, 1, 13
+    outs = {}
+    for name, env in (("free", {}), ("capped", {"HB_LANE_SMS": "1,2,3,5"})):
+        out = tmp_path / f"tick_{name}.npz"
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, WIDE))], check=True, env=dict(os.environ, **env),
+                       timeout=600)
+        outs[name] = np.load(out)
+    for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+        assert np.array_equal(outs["capped"][k], outs["free"][k]), k
