@@ -221,7 +221,12 @@ __device__ __forceinline__ void issue_groups(const ConvArgs& a, uint32_t d_tmem,
   }
 }
 
-template <int F, bool kPair>
+// kHalf (pair mode only): M = 128 over the pair, 64 output positions per CTA, for
+// layers whose whole output fits 64 rows per bed (the 1024-channel L = 59 / 30
+// layers: two beds per pair instead of one bed per 128-row tile).  The UMMA
+// 2-SM M=128 accumulator is laid out 64 rows x N in two halves: TMEM lanes
+// 0-63 hold columns [0, N/2), lanes 64-127 columns [N/2, N) of the same rows.
+template <int F, bool kPair, bool kHalf = false>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ ConvArgs a) {
@@ -411,7 +416,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // -------------------------------------------------------------- MMA issuer
     // The whole warp walks the loop with warp-uniform values (kept in uniform
     // registers); one elected lane issues each tcgen05.mma / commit.
-    const uint32_t idesc = make_idesc_f16(kPair ? 2 * kBM : kBM, a.bnp);
+    const uint32_t idesc = make_idesc_f16(kPair ? (kHalf ? kBM : 2 * kBM) : kBM, a.bnp);
+    const int acc_cols = kHalf ? a.bnp / 2 : a.bnp;  // TMEM columns per accumulator
     const uint32_t a_lbo = (a.ck >= 16) ? static_cast<uint32_t>(a.rows * 16) : 16u;
     const int b_n = kPair ? a.bnp / 2 : a.bnp;  // B rows held by this CTA
     const uint32_t b_lbo = static_cast<uint32_t>(b_n * 16);
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_wait(&acc_empty[acc], accph ^ 1, 10 + 1000 * static_cast<int>(bres_ph));
       if (prof) t_acc += clock64() - t0;
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * a.bnp);
+      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * acc_cols);
       for (int kc = 0; kc < a.n_kchunks; ++kc) {
         const int slot = a.b_resident ? kc : bs;
         if (prof) t0 = clock64();
@@ -537,7 +543,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // -------------------------------------------------------------- epilogue
     const int eg = (static_cast<int>(warp) - 4) >> 2;  // epilogue warpgroup = accumulator buffer
     const int wq = static_cast<int>(warp) & 3;          // TMEM lane quadrant of this warp
-    const int r = wq * 32 + static_cast<int>(lane);
+    const int r_lane = wq * 32 + static_cast<int>(lane);
+    const int r = kHalf ? (r_lane & 63) : r_lane;         // output row of this thread
+    const int chalf = kHalf ? (r_lane >> 6) : 0;          // kHalf: which half of the N tile's channels
     const int acc = eg;
     uint32_t accph = 0;
     const int out_groups = a.cout / 8;
@@ -564,8 +572,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const bool own = r < a.stride_m;  // rows past stride_m belong to the next tile (folded taps)
       const bool valid = own && l < a.lout;
       const bool in_buf = own && l < a.out_rows;
-      const int g0 = nt * (a.bn / 8);
-      const int ng = min(a.bn / 8, out_groups - g0);
+      const int g0 = nt * (a.bn / 8) + chalf * (a.bn / 16);
+      const int ng = min(kHalf ? a.bn / 16 : a.bn / 8, out_groups - g0);
       // Shortcut rows are independent of the accumulator: fetch the first 8
       // groups while the MMAs of this tile are still running.
       // identity: block input in I layout; maxpool: block input in S layout,
@@ -579,11 +587,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           rres[j] = res_row(a, static_cast<size_t>(p) * res_groups + g, l);
         }
       }
-      const float* bias_t = smem_bias ? s_bias + ti.g * a.bn
+      const int coff = chalf * (a.bn / 2);  // kHalf: this thread's channels start half an N tile in
+      const float* bias_t = smem_bias ? s_bias + ti.g * a.bn + coff
                                       : a.bias + static_cast<size_t>(ti.g) * a.bias_stride +
-                                            static_cast<size_t>(nt) * a.bn;
-      const float* fc_t = smem_bias ? s_fc + ti.g * a.bn
-                                    : a.fc_w + static_cast<size_t>(ti.g) * a.cout + static_cast<size_t>(nt) * a.bn;
+                                            static_cast<size_t>(nt) * a.bn + coff;
+      const float* fc_t = smem_bias ? s_fc + ti.g * a.bn + coff
+                                    : a.fc_w + static_cast<size_t>(ti.g) * a.cout + static_cast<size_t>(nt) * a.bn + coff;
       if (eprof) et0 = clock64();
       mbar_wait(&acc_full[acc], accph, 20 + 1000 * mt);
       if (eprof) {
@@ -592,12 +601,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         et0 = t1;
       }
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(acc * a.bnp);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(wq * 32) << 16) +
+                             static_cast<uint32_t>(acc * (kHalf ? a.bnp / 2 : a.bnp));
       float head = 0.f;
       // Rounds of up to 32 output channels: all TMEM loads of a round are
       // issued before one wait; after the last round's loads the accumulator
       // is released, so the next tile's MMAs overlap this tile's math/stores.
       const int nrounds = (ng + 3) >> 2;
+      if (nrounds <= 0) acc_release<kPair>(&acc_empty[acc], release_cl);  // (kHalf: no channels in this half)
 #pragma unroll
       for (int q = 0; q < 8; ++q) {  // unrolled: the shortcut registers are indexed statically
         if (q >= nrounds) break;
@@ -897,6 +908,13 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   a.fold = conv_fold(cin, cout, stride);
   a.bnp = a.fold * a.bn;
   a.stride_m = conv_stride_m(a.fold);
+  a.pair = conv_pair(cin, cout, stride) ? 1 : 0;
+  {  // half pairs: M = 128 over the pair (64 rows per CTA) when a bed's whole output fits 64 rows;
+    // not on a member's last conv, whose fused head sums keep the single-CTA grouping
+    static const int half_on = getenv("HB_K4_HALF") ? atoi(getenv("HB_K4_HALF")) : 1;
+    a.half = (half_on && a.pair && fc_w == nullptr && a.out_rows <= kBM / 2) ? 1 : 0;
+    if (a.half) a.stride_m = kBM / 2;
+  }
   const int ksteps = (a.ck >= 16) ? a.ck / a.fold : 8;
   a.mt_per_p = (a.out_rows + a.stride_m - 1) / a.stride_m;
   a.num_tiles = a.n_ntiles * P * a.mt_per_p;
@@ -907,7 +925,6 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   const uint32_t budget = kSmemLimit - fixed;
   const uint32_t b_all = a.b_chunk_bytes * a.n_kchunks;
   a.b_resident = resident;
-  a.pair = conv_pair(cin, cout, stride) ? 1 : 0;
   a.b_slot_bytes = a.pair ? a.b_chunk_bytes / 2 : a.b_chunk_bytes;
   a.mtp_per_p = (Pm * a.mt_per_p + 1) / 2;               // pairs per (member, N tile)
   if (a.pair) a.num_tiles = G * a.n_ntiles * a.mtp_per_p;  // M-tile pairs
@@ -927,7 +944,7 @@ const char* plan_conv(ConvPlan* plan, int G, int Pm, int cin, int cout, int lin,
   if (a.na_stages > max_stages) a.na_stages = max_stages;
   if (a.na_stages < 2) return "conv: k-chunk does not fit in shared memory";
   uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(2 * a.bnp)) cols <<= 1;
+  while (cols < static_cast<uint32_t>(a.half ? a.bnp : 2 * a.bnp)) cols <<= 1;
   a.tmem_cols = cols;
   a.wpack = wpack;
   a.wpack_stride = wpack_bytes(cin, cout);
@@ -994,6 +1011,9 @@ cudaError_t init_conv_kernel() {
     e = cudaFuncSetAttribute(conv_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(conv_tc_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(conv_tc_kernel<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemLimit);
   return e;
 }
 
@@ -1019,6 +1039,8 @@ cudaError_t launch_conv(const ConvPlan& plan, cudaStream_t st) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  if (plan.args.pair && plan.args.half)
+    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1, true, true>, plan.tmap, plan.tmapB, plan.args);
   if (plan.args.pair) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1, true>, plan.tmap, plan.tmapB, plan.args);
   if (plan.args.fold == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<2, false>, plan.tmap, plan.tmapB, plan.args);
   return cudaLaunchKernelEx(&cfg, conv_tc_kernel<1, false>, plan.tmap, plan.tmapB, plan.args);

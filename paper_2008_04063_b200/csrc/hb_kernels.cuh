@@ -88,6 +88,7 @@ struct ConvArgs {
   unsigned long long* prof;        // dbg & 8: per-CTA role cycle counters [grid][8]
   int pair;                        // CTA pairs (cta_group::2, M = 256 = two M tiles, B split along N)
   int mtp_per_p;                   // pair mode: M-tile pairs per (member, N tile) (num_tiles counts pairs)
+  int half;                        // pair mode with M = 128 over the pair: 64 output rows per CTA
   uint32_t b_slot_bytes;           // B bytes per slot in this CTA (pair mode: half a k-chunk's image)
 };
 
