@@ -309,6 +309,32 @@ def test_k4_cta_pairs_bit_identical(tmp_path):
     _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
 
 
+DEEP = [15, 19]   # w64-d16 (512-channel L = 59 / 30 layers), w128-d16 (1024-channel L = 59 / 30 layers)
+
+
+def test_k4_half_pairs_bit_identical(tmp_path):
+    """K4 half pairs (HB_K4_HALF=1: M = 128 over the CTA pair, 64 output rows per CTA, two beds per
+    pair) on the deep layers whose output fits 64 rows per bed, against full 256-row pairs: every
+    output element sees the same MMA sequence, so the ticks are bit-identical; both match the
+    oracle.  An odd bed count leaves the last pair's second half past the layer."""
+    P, hop, ticks, seed = 3, 250, 1, 14
+    outs = {}
+    for half in ("0", "1"):
+        out = tmp_path / f"tick{half}.npz"
+        e = dict(os.environ, HB_K4_HALF=half)
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, DEEP))], check=True, env=e, timeout=600)
+        outs[half] = np.load(out)
+    for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+        assert np.array_equal(outs["1"][k], outs["0"][k]), k
+    got = outs["1"]
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = list(range(P))
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, DEEP), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
+
+
 def test_k4_cta_pairs_under_lane_caps(tmp_path):
     """CTA-pair K4 launches inside SM-capped lanes (HB_LANE_SMS=1,2,3,5: a lane below two SMs still
     gets one cluster; odd caps round down to whole pairs): bit-identical to the uncapped tick."""
