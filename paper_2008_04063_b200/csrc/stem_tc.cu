@@ -325,6 +325,7 @@ struct StemPPArgs {
   int G, Pm, L, C, Ceff, pad, out_qs, out_lq, out_rows;
   int J, dd, paired, groups_per_blk, nt_per_row, num_tiles, n_stages;
   int dbg;  // HB_STEM_DBG (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA
+  int ug;   // epilogue units per TMEM load set: 4 (x32, one set; the default where it divides) or 1 (x8, two sets)
   __half* out;
   unsigned* flags;  // per tile counter (+1 per column half after its stores), null = none (see launch_stems)
 };
@@ -538,7 +539,7 @@ __global__ void __launch_bounds__(kStemPPThreads, 1) stem_pp_kernel(const __grid
         tmem_ld8_nw(ca, ra);
         tmem_ld8_nw(cb, rb);
       };
-      auto store = [&](int u, const uint32_t (&ra)[8], const uint32_t (&rb)[8]) {
+      auto store = [&](int u, const uint32_t* ra, const uint32_t* rb) {
         const int code = sUnit[u];
         const int ja = code & 255, c8 = code >> 8, jb = ja + a.dd;
         const float4 b0 = *reinterpret_cast<const float4*>(sBias + g * a.Ceff + c8 * 8);
@@ -568,24 +569,40 @@ __global__ void __launch_bounds__(kStemPPThreads, 1) stem_pp_kernel(const __grid
         tc_fence_before();
         mbar_arrive(&acc_empty[eb]);
       };
-      uint32_t xa[8], xb[8], ya[8], yb[8];
-      if (u_lo < u_hi) issue(u_lo, xa, xb);
-      for (int u = u_lo; u < u_hi; u += 2) {
-        tmem_wait_ld();  // set x (unit u) landed
-        if (u + 1 < u_hi) {
-          issue(u + 1, ya, yb);
-        } else {
-          release();
+      if (a.ug == 4) {
+        // four units (one phase pair, 32 consecutive columns per phase) per load
+        // set: two waits per tile instead of eight
+        uint32_t ra[32], rb[32];
+        for (int u = u_lo; u < u_hi; u += 4) {
+          uint32_t ca, cb;
+          unit_cols(u, ca, cb);
+          tmem_ld32_nw(ca, ra);
+          tmem_ld32_nw(cb, rb);
+          tmem_wait_ld();
+          if (u + 4 >= u_hi) release();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) store(u + k, ra + 8 * k, rb + 8 * k);
         }
-        store(u, xa, xb);
-        if (u + 1 >= u_hi) break;
-        tmem_wait_ld();  // set y (unit u + 1) landed
-        if (u + 2 < u_hi) {
-          issue(u + 2, xa, xb);
-        } else {
-          release();
+      } else {
+        uint32_t xa[8], xb[8], ya[8], yb[8];
+        if (u_lo < u_hi) issue(u_lo, xa, xb);
+        for (int u = u_lo; u < u_hi; u += 2) {
+          tmem_wait_ld();  // set x (unit u) landed
+          if (u + 1 < u_hi) {
+            issue(u + 1, ya, yb);
+          } else {
+            release();
+          }
+          store(u, xa, xb);
+          if (u + 1 >= u_hi) break;
+          tmem_wait_ld();  // set y (unit u + 1) landed
+          if (u + 2 < u_hi) {
+            issue(u + 2, xa, xb);
+          } else {
+            release();
+          }
+          store(u + 1, ya, yb);
         }
-        store(u + 1, ya, yb);
       }
       if (u_lo >= u_hi) {  // no units for this warpgroup: release the buffer all the same
         tc_fence_before();
@@ -649,6 +666,12 @@ static cudaError_t plan_stem_pp(const StemGroup& sg, std::vector<StemPPSub>* sub
   a.nt_per_row = ((a.out_rows + 1023) / 1024) * a.groups_per_blk;
   a.n_stages = kStemPPStages;
   a.dbg = getenv("HB_STEM_DBG") ? atoi(getenv("HB_STEM_DBG")) : 0;
+  {  // units per TMEM load set (HB_STEM_UG): a warpgroup's units must split into whole sets of one phase pair
+    // (measured, zero data: w32 group 64 beds 24.9 -> 23.1 us, 1024 beds 101 -> 91 us; c2 tick -0.8 %)
+    const int want = getenv("HB_STEM_UG") ? atoi(getenv("HB_STEM_UG")) : 4;
+    const int nc8 = cout / 8, units = (a.J / 2) * nc8;
+    a.ug = (want == 4 && nc8 % 4 == 0 && units % 4 == 0 && ((units + 1) / 2) % 4 == 0) ? 4 : 1;
+  }
   // members per launch: every member's 16 B images stay resident
   const size_t per_g = static_cast<size_t>(16) * a.Ceff * 32 + a.Ceff * 4 + static_cast<size_t>(cout) * kTaps * 4;
   const size_t fixed = static_cast<size_t>(a.n_stages) * kStemSeg + (2 * a.n_stages + 4) * 8 + 16 + 64 * 4;
