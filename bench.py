@@ -667,7 +667,7 @@ def run_b200(args):
             "ingest_window": float(ms[kinds == 0].sum()), "stem": float(ms[kinds == 1].sum()),
             "conv_tcgen05": conv_ms, "conv_k4c_chain": ch_ms, "conv_k4b": pp_ms, "conv_k4": tc_ms,
             "aggregate": float(ms[kinds == 3].sum() + ms[kinds == 4].sum()), "total": tick_ms_eager},
-        "tick_path": ("K4c chain: window, stems (one launch), ONE persistent conv launch, aggregate"
+        "tick_path": ("K4c chain: window, stems (one launch), ONE persistent conv launch with the ensemble aggregation fused in"
                       if ch_n else "per-layer: one K4/K4b launch per conv layer, member lanes in graph branches"),
         "tick_launches": [int(x) for x in kinds],
         "tick_flops": float(flops.sum()),

@@ -571,6 +571,67 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// K5's aggregation of one bed, by one warp, in K5's arithmetic order (per member: lane-strided
+// partial sums, xor-shuffle reduction, fc bias; then the members left to right): the fused and the
+// separate aggregation are bit-identical.  The partials were written by other CTAs in this launch
+// (published through the bed counter's acquire): read through L2.
+__device__ __forceinline__ void chain_aggregate_bed(const ChainArgs& ca, int bed, int lane) {
+  const HeadMember* heads = static_cast<const HeadMember*>(ca.heads);
+  const int M = ca.n_heads;
+  float sp = 0.f, sl = 0.f;
+  // members in batches of 8 whose partial loads are all in flight at once (a bed's partials sit in
+  // L2: one round trip per batch instead of one per member); up to 64 partials per member a lane
+  // holds its (at most two) terms of K5's strided sum, added in K5's order
+  for (int m0 = 0; m0 < M; m0 += 8) {
+    const int nm = M - m0 < 8 ? M - m0 : 8;
+    HeadMember hm[8];
+    float va[8], vb[8];
+    bool small = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < nm) {
+        hm[k] = heads[m0 + k];
+        small = small && hm[k].mt <= 64;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      va[k] = vb[k] = 0.f;
+      if (small && k < nm) {
+        const float* src = hm[k].partial + static_cast<size_t>(bed) * hm[k].mt;
+        if (lane < hm[k].mt) va[k] = __ldcg(src + lane);
+        if (lane + 32 < hm[k].mt) vb[k] = __ldcg(src + lane + 32);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= nm) break;
+      float s = 0.f;
+      if (small) {
+        if (lane < hm[k].mt) s += va[k];
+        if (lane + 32 < hm[k].mt) s += vb[k];
+      } else {
+        const float* src = hm[k].partial + static_cast<size_t>(bed) * hm[k].mt;
+        for (int i = lane; i < hm[k].mt; i += 32) s += __ldcg(src + i);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const float lg = hm[k].fc_b + s * hm[k].inv_len;
+      if (lane == 0) {
+        ca.member_logits[static_cast<size_t>(bed) * M + m0 + k] = lg;
+        sp += 1.f / (1.f + expf(-lg));
+        sl += lg;
+      }
+    }
+  }
+  if (lane == 0) {
+    ca.ens_prob[bed] = sp / static_cast<float>(M);
+    ca.ens_logit[bed] = sl / static_cast<float>(M);
+    ca.ens_sums[bed] = sp;
+    ca.ens_sums[ca.P + bed] = sl;
+  }
+}
+
 // Wait until the counters [a0, a1) and [b0, b1) (at most kMaxRange each) reached
 // `target`: all read in one batch of independent acquire loads (one L2 round
 // trip), registers only, re-polled with a short sleep while any is short.
@@ -872,6 +933,23 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
       pr[7] = m_st;
       pr[8] = clock64() - m_start;
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------- aggregation
+    // (fused K5) beds blockIdx.x, + gridDim.x, ...: once a bed's head-tile halves are all counted
+    // (bed_target per launch, counters never reset) its members' partials are summed and the
+    // bed's outputs written.  Every CTA of the persistent grid is resident, so the wait ends.
+    if (ca.agg) {
+      if (!ca.stems_flagged) pdl_wait();
+      const uint32_t target = ca.bed_target * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
+      for (int p = static_cast<int>(blockIdx.x); p < ca.P; p += static_cast<int>(gridDim.x)) {
+        uint32_t spins = 0;
+        while (!__all_sync(0xffffffffu, static_cast<int>(ld_acquire_u32(ca.bed_ctr + p) - target) >= 0)) {
+          __nanosleep(128);
+          if (++spins == (1u << 26)) asm volatile("trap;");  // a head tile that never lands is a planning bug
+        }
+        chain_aggregate_bed(ca, p, static_cast<int>(lane));
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ epilogue
     const int ew = (static_cast<int>(warp) - 4) >> 2;
@@ -914,6 +992,12 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
           __threadfence();
           red_release_add_u32(ca.flags + ca.flag_base[li] + tile, 1u);
         }
+      } else if (ca.agg) {  // a head tile's half: count it for the bed (warp 3 of the bed's CTA aggregates)
+        named_bar_sync(2 + ew, 128);  // the warpgroup's head partials are stored
+        if (wq == 0 && lane == 0) {
+          __threadfence();
+          red_release_add_u32(ca.bed_ctr + (t.p - t.g * a.Pm), 1u);
+        }
       }
       if (ca.trace && wq == 0 && lane == 0) ca.trace[5 * gi + 3 + half] = globaltimer();
       if (prof) e_work += clock64() - e0;
@@ -934,6 +1018,7 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     if (atomicAdd(ca.sync + 1, 1u) == gridDim.x - 1) {
       for (int k = 0; k < ca.n_chains; ++k) ca.ctr[k] = 0u;
       ca.sync[1] = 0u;
+      if (ca.agg && ca.wpos != nullptr) *ca.wpos += ca.advance;  // the tick's ring cursor (K5's job otherwise)
       __threadfence();
       atomicAdd(ca.sync, 1u);
     }
@@ -1208,6 +1293,7 @@ void free_chain(ChainPlan* cp) {
   cudaFree(cp->d_sync);
   cudaFree(cp->d_prof);
   cudaFree(cp->d_trace);
+  cudaFree(cp->d_bed);
   cudaFree(cp->d_idesc);
   cudaFree(cp->d_ideps);
   delete cp->args;

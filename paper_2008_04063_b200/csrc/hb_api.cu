@@ -361,6 +361,7 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
       CK(c, cudaStreamWaitEvent(st, c->ev[1 + ln], 0));
     }
   }
+  if (c->chain_on && c->chain.args->agg) return HB_OK;  // aggregation and cursor advance fused into K4c
   CK(c, launch_aggregate(c->d_heads, static_cast<int>(c->selected.size()), c->P, c->member_logits, c->ens_prob,
                          c->ens_logit, c->ens_sums, c->wpos, c->hop, st));
   {  // algorithmic bytes: every member's head partials in, member logits + 2 ensemble outputs + 2 sums out
@@ -641,6 +642,31 @@ int build_selection(hb_ctx* c) {
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
   CK(c, cudaMemcpy(c->d_heads, heads.data(), sizeof(HeadMember) * heads.size(), cudaMemcpyHostToDevice));
+  if (c->chain_on) {  // ensemble aggregation fused into the chain launch (HB_CHAIN_AGG=0: K5 after it)
+    ChainArgs& ca = *c->chain.args;
+    const char* ag = getenv("HB_CHAIN_AGG");
+    ca.agg = (ag ? atoi(ag) : 1) != 0 ? 1 : 0;
+    if (ca.agg) {
+      unsigned target = 0;  // head-tile halves per bed: every member's last conv, per column tile
+      for (int i = 0; i < c->chain.n_layers; ++i)
+        if (ca.L[i].fc_w != nullptr) target += static_cast<unsigned>(ca.L[i].G * ca.L[i].nt_per_p * kEpiPartsChain);
+      ca.n_heads = M;
+      ca.P = c->P;
+      ca.heads = c->d_heads;
+      ca.member_logits = c->member_logits;
+      ca.ens_prob = c->ens_prob;
+      ca.ens_logit = c->ens_logit;
+      ca.ens_sums = c->ens_sums;
+      ca.wpos = c->wpos;
+      ca.advance = c->hop;
+      ca.bed_target = target;
+      if (!c->chain.d_bed) {
+        CK(c, cudaMalloc(&c->chain.d_bed, sizeof(unsigned) * c->P));
+        CK(c, cudaMemset(c->chain.d_bed, 0, sizeof(unsigned) * c->P));
+      }
+      ca.bed_ctr = c->chain.d_bed;
+    }
+  }
   // capture the tick into a graph
   cudaStream_t cap;
   CK(c, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));

@@ -168,6 +168,21 @@ struct ChainArgs {
   unsigned long long* prof;        // HB_CHAIN_PROF: per CTA [16] role cycle counters (null = off)
   unsigned long long* trace;       // HB_CHAIN_PROF: per queue item [5] globaltimer ns: pulled, weights in place,
                                    // dependencies met, column half 0 / 1 published
+  // Ensemble aggregation fused into the chain (agg != 0; else K5 runs after it): the warp whose head-tile
+  // half completes a bed (per-bed counter reaches bed_target * (epoch + 1)) sums every member's head
+  // partials of that bed in K5's order and writes the bed's outputs; the last CTA out advances the ring
+  // cursor.  heads is a `const HeadMember*` (declared below).
+  int agg;
+  int n_heads, P;                  // members (selection order), beds
+  const void* heads;
+  float* member_logits;            // [P][n_heads]
+  float* ens_prob;
+  float* ens_logit;
+  float* ens_sums;                 // [2][P]
+  long long* wpos;
+  int advance;
+  unsigned* bed_ctr;               // [P], never reset (epoch-relative targets)
+  unsigned bed_target;             // head-tile halves per bed per launch
 };
 struct ChainLayerIn {
   const struct PPPlan* plan;
@@ -188,6 +203,7 @@ struct ChainPlan {
   unsigned* d_sync = nullptr;
   unsigned long long* d_prof = nullptr;
   unsigned long long* d_trace = nullptr;
+  unsigned* d_bed = nullptr;       // per-bed head counters (fused aggregation)
   int4* d_idesc = nullptr;
   int4* d_ideps = nullptr;
   std::vector<unsigned*> stem_flags;  // per chain: its stem's tile counters (inside d_flags), when flagged

@@ -175,13 +175,39 @@ def test_k4c_chain_capped_grid(monkeypatch, chain_sms):
 
 def test_k4c_chain_is_the_c2_tick():
     """The benchmark's c2 selection runs as the window kernel, ONE stem launch for both member
-    groups, ONE chain launch (kind 6) and the aggregate: four launches per tick."""
+    groups and ONE chain launch (kind 6) with the ensemble aggregation fused in: three launches per
+    tick (HB_CHAIN_AGG=0 adds the separate aggregate kernel, kind 3)."""
     from paper_2008_04063_b200.engine import EnsembleEngine
     zoo = holmes_zoo()
     with EnsembleEngine(zoo, Selector.from_indices(60, C2), 8, hop=250) as eng:
         eng.ingest(synth.ecg_block(0, 8, 3, 0, W))
         kinds = eng.profile_tick()[0].tolist()
-    assert kinds == [0, 1, 6, 3], kinds
+    assert kinds == [0, 1, 6], kinds
+
+
+@pytest.mark.parametrize("P,extra", [(64, {}), (16, {"HB_CHAIN_SMS": "5"}), (9, {"HB_CHAIN_SMS": "2"})])
+def test_chain_fused_aggregation_bit_identical(tmp_path, P, extra):
+    """Aggregation fused into the K4c launch (warp 3 of CTA p mod grid sums bed p's head partials
+    once the bed's per-launch head-tile count is reached; the last CTA out advances the ring
+    cursor) against the separate aggregate kernel (HB_CHAIN_AGG=0): bit-identical over three
+    sliding ticks (the cursor and the epoch-relative counters carry across ticks), with capped
+    grids where one CTA aggregates several beds; both match the oracle."""
+    hop, ticks, seed = 250, 3, 15
+    outs = {}
+    for agg in ("0", "1"):
+        out = tmp_path / f"tick{agg}.npz"
+        e = dict(os.environ, HB_CHAIN="1", HB_CHAIN_AGG=agg, **extra)
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, C2))], check=True, env=e, timeout=600)
+        outs[agg] = np.load(out)
+    for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+        assert np.array_equal(outs["1"][k], outs["0"][k]), k
+    got = outs["1"]
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = sorted({0, P // 2, P - 1})
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, C2), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
 
 
 def test_k4b_group_caps(monkeypatch):
