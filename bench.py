@@ -658,6 +658,9 @@ def run_b200(args):
         from paper_2008_04063_b200.zoo import Selector
         extras["c3_full_zoo_100_beds"] = tick_at(zoo, Selector.ones(60), 100, hop, local, K=50, warm=3,
                                                  e2e_ticks=20)
+        # BASELINE c1: one member (ecg-i-w32-d8, as tests/test_parity_timed_gpu.py::test_c1) for one bed
+        extras["c1_one_member_one_bed"] = tick_at(zoo, Selector.from_indices(60, [10]), 1, hop, local, K=200,
+                                                  e2e_ticks=100)
         extras["profiler_sweep"] = sweep_bench(local)
 
     roof = tick_roofline(zoo, eng.selector, P, peak_tf, peak_hbm)
