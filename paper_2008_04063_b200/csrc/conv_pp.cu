@@ -575,7 +575,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // partial sums, xor-shuffle reduction, fc bias; then the members left to right): the fused and the
 // separate aggregation are bit-identical.  The partials were written by other CTAs in this launch
 // (published through the bed counter's acquire): read through L2.
-__device__ __forceinline__ void chain_aggregate_bed(const ChainArgs& ca, int bed, int lane) {
+__device__ __forceinline__ void chain_aggregate_bed(const ChainArgs& ca, int bed /* global */, int lane) {
   const HeadMember* heads = static_cast<const HeadMember*>(ca.heads);
   const int M = ca.n_heads;
   float sp = 0.f, sl = 0.f;
@@ -935,19 +935,19 @@ __global__ void __launch_bounds__(kPPThreads, 1) chain_pp_kernel(const __grid_co
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------- aggregation
-    // (fused K5) beds blockIdx.x, + gridDim.x, ...: once a bed's head-tile halves are all counted
+    // (fused K5) chunk beds blockIdx.x, + gridDim.x, ...: once a bed's head-tile halves are all counted
     // (bed_target per launch, counters never reset) its members' partials are summed and the
     // bed's outputs written.  Every CTA of the persistent grid is resident, so the wait ends.
     if (ca.agg) {
       if (!ca.stems_flagged) pdl_wait();
       const uint32_t target = ca.bed_target * (*reinterpret_cast<volatile unsigned*>(ca.sync) + 1u);
-      for (int p = static_cast<int>(blockIdx.x); p < ca.P; p += static_cast<int>(gridDim.x)) {
+      for (int p = static_cast<int>(blockIdx.x); p < ca.n_beds; p += static_cast<int>(gridDim.x)) {
         uint32_t spins = 0;
         while (!__all_sync(0xffffffffu, static_cast<int>(ld_acquire_u32(ca.bed_ctr + p) - target) >= 0)) {
           __nanosleep(128);
           if (++spins == (1u << 26)) asm volatile("trap;");  // a head tile that never lands is a planning bug
         }
-        chain_aggregate_bed(ca, p, static_cast<int>(lane));
+        chain_aggregate_bed(ca, ca.bed0 + p, static_cast<int>(lane));
       }
     }
   } else if (warp >= 4) {

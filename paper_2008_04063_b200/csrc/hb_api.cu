@@ -151,6 +151,7 @@ struct hb_ctx {
   // patient micro-batching: member chains run over chunks of Pc beds so the
   // activation buffers stay within act_budget (the rings / windows hold all P)
   int Pc = 0, n_chunks = 1, P_pad = 0;
+  int chain_pc = 0;                    // beds per K4c launch (chain mode)
   double act_budget = 64e9;
   cudaStream_t own = nullptr;
   float* ring = nullptr;
@@ -194,7 +195,8 @@ struct hb_ctx {
   // inside a tick, so no write-after-read hazard between tiles)
   bool chain_on = false;
   int stem_sms = 0;  // chain mode: CTAs of the stem launch (0 = one per SM); the chain takes the other SMs first
-  ChainPlan chain;
+  ChainPlan chain;                    // K4c over bed chunk 0 (the only chunk up to HB_CHAIN_MAX_P beds)
+  std::vector<ChainPlan> chain_rest;  // K4c over bed chunks 1.. (bed counts above HB_CHAIN_MAX_P)
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // bracket the last tick graph launch
   bool timed = false;
@@ -230,6 +232,8 @@ void free_selection(hb_ctx* c) {
   for (auto& a : c->act) cudaFree(a);
   c->act.clear();
   free_chain(&c->chain);
+  for (auto& cp : c->chain_rest) free_chain(&cp);
+  c->chain_rest.clear();
   c->chain_on = false;
   for (auto& g : c->groups) {
     for (auto p : g.cbuf) cudaFree(p);
@@ -300,14 +304,16 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
   // the aggregate (captured as parallel graph branches).  The eager profiling
   // path (pr->ev set) keeps everything on one stream so per-kernel event times
   // stay clean.
-  if (c->chain_on) {  // every group's stem in one launch, then every group's conv chain in one launch
+  for (int ch = 0; c->chain_on && ch < c->n_chunks; ++ch) {
+    // every group's stem in one launch, then every group's conv chain in one launch, per bed chunk
+    const ChainPlan& cp = ch == 0 ? c->chain : c->chain_rest[ch - 1];
     std::vector<StemGroup> sg;
     for (size_t gi = 0; gi < c->groups.size(); ++gi) {
       const Group& g = c->groups[gi];
       const LayerSpec& s0 = g.layers[0];
-      sg.push_back({g.stem[0].data(), static_cast<int>(g.mi.size()), round_up(c->W, 8), c->Pc, c->W,
+      sg.push_back({g.stem[ch].data(), static_cast<int>(g.mi.size()), round_up(c->W, 8), c->Pc, c->W,
                     layer_in_q(g.layers[1], g.kind[1]), s0.cout, s0.pad, g.cbuf[0],
-                    c->chain.stem_flags.empty() ? nullptr : c->chain.stem_flags[gi]});
+                    cp.stem_flags.empty() ? nullptr : cp.stem_flags[gi]});
     }
     // one launch for every group's stem, in the graph and in the eager profile alike
     CK(c, launch_stems(sg.data(), static_cast<int>(sg.size()), c->stem_sms, st));
@@ -321,8 +327,8 @@ int enqueue_tick(hb_ctx* c, cudaStream_t st, ProfRec* pr = nullptr) {
       }
       pr->mark(st, K_STEM, fl, by);
     }
-    CK(c, launch_chain(c->chain, st));
-    pr->mark(st, K_CHAIN, c->chain.flops, c->chain.bytes);
+    CK(c, launch_chain(cp, st));
+    pr->mark(st, K_CHAIN, cp.flops, cp.bytes);
   }
   const bool fork = !c->chain_on && (pr->ev == nullptr) && c->lanes > 1;
   if (fork) CK(c, cudaEventRecord(c->ev[0], st));
@@ -449,9 +455,19 @@ int build_selection(hb_ctx* c) {
         }
         if (!L.head) bytes += static_cast<double>(c->P) * g.mi.size() * L.cout * plane_rows_max(L.lout) * sizeof(__half);
       }
-    c->chain_on = ok && n_layers <= kMaxChainLayers && bytes <= c->act_budget;
+    // HB_CHAIN_CHUNK_P=n: above HB_CHAIN_MAX_P beds run the chain over bed chunks of n (one chain
+    // launch per chunk, buffers reused).  Default 0 (off): measured slower than the per-layer
+    // launches at every bed count tried (tools/gpu_chunkchain.sh, abtick: 1024 beds 9.38 ms per-layer
+    // vs 10.12 / 10.67 / 10.31 ms in chunks of 64 / 96 / 128 and 9.96 ms as one launch; 192-512 alike)
+    const int chunk_p = getenv("HB_CHAIN_CHUNK_P") ? atoi(getenv("HB_CHAIN_CHUNK_P")) : 0;
+    const bool chunked = chunk_p > 0 && c->P > max_p && chunk_p < c->P;
+    ok = ok || (chain_mode < 0 && chunked && !(dbg && atoi(dbg)) && c->P >= min_p);
+    for (auto& g : c->groups)
+      for (size_t li = 1; li < g.layers.size(); ++li) ok = ok && g.kind[li] == KIND_PP;
+    c->chain_on = ok && n_layers <= kMaxChainLayers && bytes * (chunked ? double(chunk_p) / c->P : 1.0) <= c->act_budget;
+    c->chain_pc = c->chain_on && chunked ? chunk_p : c->P;
   }
-  c->Pc = c->P;
+  c->Pc = c->chain_on ? c->chain_pc : c->P;
   while (!c->chain_on && c->Pc > 1 && size_for(c->Pc) > c->act_budget) c->Pc = (c->Pc + 1) / 2;
   size_for(c->Pc);
   c->n_chunks = (c->P + c->Pc - 1) / c->Pc;
@@ -485,7 +501,7 @@ int build_selection(hb_ctx* c) {
     if (c->chain_on)
       for (size_t li = 0; li + 1 < g.layers.size(); ++li) {
         const LayerSpec& L = g.layers[li];
-        const size_t b = static_cast<size_t>(c->P) * G * L.cout * plane_rows_max(L.lout) * sizeof(__half);
+        const size_t b = static_cast<size_t>(c->Pc) * G * L.cout * plane_rows_max(L.lout) * sizeof(__half);
         __half* p = nullptr;
         CK(c, cudaMalloc(&p, b));
         CK(c, cudaMemset(p, 0, b));
@@ -601,7 +617,7 @@ int build_selection(hb_ctx* c) {
     // default off: the stem and the first layers share one HBM-bound phase, so overlapping them
     // measured no gain (tools/abtick.py: 0.626 ms whole-launch wait vs 0.639-0.709 ms with counters,
     // stem grids of 32-148 CTAs)
-    bool flag_stems = (sf ? atoi(sf) : 0) != 0 && (hs ? atoi(hs) : 1) != 0;
+    bool flag_stems = (sf ? atoi(sf) : 0) != 0 && (hs ? atoi(hs) : 1) != 0 && c->n_chunks == 1;
     std::vector<ChainStemIn> stems;
     for (const Group& g : c->groups) {
       const LayerSpec& s0 = g.layers[0];
@@ -612,59 +628,66 @@ int build_selection(hb_ctx* c) {
       stems.push_back({tpr, tpr / blocks, act_rows_q(c->W, oq), c->Pc * static_cast<int>(g.mi.size())});
     }
     c->stem_sms = flag_stems ? (getenv("HB_STEM_SMS") ? atoi(getenv("HB_STEM_SMS")) : 0) : 0;
-    std::vector<ChainLayerIn> cl;
-    double flops = 0, bytes = 0;
-    for (size_t gi = 0; gi < c->groups.size(); ++gi) {
-      const Group& g = c->groups[gi];
-      const int first = static_cast<int>(cl.size());
-      const double rows = static_cast<double>(c->P) * g.mi.size();
-      for (size_t li = 1; li < g.layers.size(); ++li) {
-        const LayerSpec& L = g.layers[li];
-        ChainLayerIn x;
-        x.plan = &c->plans[g.plan0[0] + li - 1].pp;
-        x.dep_in = li >= 2 ? first + static_cast<int>(li) - 2 : (flag_stems ? kChainDepStem : -1);
-        x.dep_res = (li % 2 == 0 && li >= 3) ? first + static_cast<int>(li) - 3
-                                             : (li == 2 && flag_stems ? kChainDepStem : -1);
-        x.chain = static_cast<int>(gi);
-        cl.push_back(x);
-        flops += rows * 2.0 * L.cin * L.cout * kTaps * L.lout;
-        bytes += rows * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
-                               (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0));
-      }
-    }
     int grid = c->num_sms;  // HB_CHAIN_SMS caps the persistent grid (tests: many items per CTA, stealing)
     if (const char* cs = getenv("HB_CHAIN_SMS")) grid = std::max(1, std::min(grid, atoi(cs)));
-    const char* e = plan_chain(&c->chain, cl.data(), static_cast<int>(cl.size()), grid,
-                               flag_stems ? stems.data() : nullptr);
-    if (e) return fail(c, HB_E_INVALID, e);
-    c->chain.flops = flops;
-    c->chain.bytes = bytes;
+    c->chain_rest.assign(c->n_chunks - 1, ChainPlan());
+    for (int ch = 0; ch < c->n_chunks; ++ch) {  // one chain plan per bed chunk (its head partials' rows)
+      std::vector<ChainLayerIn> cl;
+      double flops = 0, bytes = 0;
+      for (size_t gi = 0; gi < c->groups.size(); ++gi) {
+        const Group& g = c->groups[gi];
+        const int first = static_cast<int>(cl.size());
+        const double rows = static_cast<double>(c->Pc) * g.mi.size();
+        for (size_t li = 1; li < g.layers.size(); ++li) {
+          const LayerSpec& L = g.layers[li];
+          ChainLayerIn x;
+          x.plan = &c->plans[g.plan0[ch] + li - 1].pp;
+          x.dep_in = li >= 2 ? first + static_cast<int>(li) - 2 : (flag_stems ? kChainDepStem : -1);
+          x.dep_res = (li % 2 == 0 && li >= 3) ? first + static_cast<int>(li) - 3
+                                               : (li == 2 && flag_stems ? kChainDepStem : -1);
+          x.chain = static_cast<int>(gi);
+          cl.push_back(x);
+          flops += rows * 2.0 * L.cin * L.cout * kTaps * L.lout;
+          bytes += rows * 2.0 * (static_cast<double>(L.cin) * L.lin + (L.head ? 0.0 : static_cast<double>(L.cout) * L.lout) +
+                                 (L.res_mode ? static_cast<double>(L.res_c) * L.lin : 0.0));
+        }
+      }
+      ChainPlan& cp = ch == 0 ? c->chain : c->chain_rest[ch - 1];
+      const char* e = plan_chain(&cp, cl.data(), static_cast<int>(cl.size()), grid, flag_stems ? stems.data() : nullptr);
+      if (e) return fail(c, HB_E_INVALID, e);
+      cp.flops = flops;
+      cp.bytes = bytes;
+    }
   }
   CK(c, cudaMalloc(&c->d_heads, sizeof(HeadMember) * heads.size()));
   CK(c, cudaMemcpy(c->d_heads, heads.data(), sizeof(HeadMember) * heads.size(), cudaMemcpyHostToDevice));
-  if (c->chain_on) {  // ensemble aggregation fused into the chain launch (HB_CHAIN_AGG=0: K5 after it)
-    ChainArgs& ca = *c->chain.args;
+  for (int ch = 0; c->chain_on && ch < c->n_chunks; ++ch) {
+    // ensemble aggregation fused into each chunk's chain launch (HB_CHAIN_AGG=0: K5 after the last)
+    ChainPlan& cp = ch == 0 ? c->chain : c->chain_rest[ch - 1];
+    ChainArgs& ca = *cp.args;
     const char* ag = getenv("HB_CHAIN_AGG");
     ca.agg = (ag ? atoi(ag) : 1) != 0 ? 1 : 0;
     if (ca.agg) {
       unsigned target = 0;  // head-tile halves per bed: every member's last conv, per column tile
-      for (int i = 0; i < c->chain.n_layers; ++i)
+      for (int i = 0; i < cp.n_layers; ++i)
         if (ca.L[i].fc_w != nullptr) target += static_cast<unsigned>(ca.L[i].G * ca.L[i].nt_per_p * kEpiPartsChain);
       ca.n_heads = M;
       ca.P = c->P;
+      ca.bed0 = ch * c->Pc;
+      ca.n_beds = std::max(0, std::min(c->Pc, c->P - ch * c->Pc));  // (the last chunk's padding beds: none)
       ca.heads = c->d_heads;
       ca.member_logits = c->member_logits;
       ca.ens_prob = c->ens_prob;
       ca.ens_logit = c->ens_logit;
       ca.ens_sums = c->ens_sums;
-      ca.wpos = c->wpos;
+      ca.wpos = ch + 1 == c->n_chunks ? c->wpos : nullptr;  // the tick's cursor: once, by the last chunk
       ca.advance = c->hop;
       ca.bed_target = target;
-      if (!c->chain.d_bed) {
-        CK(c, cudaMalloc(&c->chain.d_bed, sizeof(unsigned) * c->P));
-        CK(c, cudaMemset(c->chain.d_bed, 0, sizeof(unsigned) * c->P));
+      if (!cp.d_bed) {
+        CK(c, cudaMalloc(&cp.d_bed, sizeof(unsigned) * c->Pc));
+        CK(c, cudaMemset(cp.d_bed, 0, sizeof(unsigned) * c->Pc));
       }
-      ca.bed_ctr = c->chain.d_bed;
+      ca.bed_ctr = cp.d_bed;
     }
   }
   // capture the tick into a graph

@@ -173,7 +173,8 @@ struct ChainArgs {
   // partials of that bed in K5's order and writes the bed's outputs; the last CTA out advances the ring
   // cursor.  heads is a `const HeadMember*` (declared below).
   int agg;
-  int n_heads, P;                  // members (selection order), beds
+  int n_heads, P;                  // members (selection order), beds of the tick
+  int bed0, n_beds;                // this launch's bed chunk: beds [bed0, bed0 + n_beds) (counters chunk-local)
   const void* heads;
   float* member_logits;            // [P][n_heads]
   float* ens_prob;

@@ -104,13 +104,16 @@ def test_c2_64_beds_every_bed_three_ticks():
     _run(Selector.from_indices(60, C2), 64, 250, 3, 0, list(range(64)), zero_bed=17)
 
 
-@pytest.mark.parametrize("chain", ["auto", "1"])
+@pytest.mark.parametrize("chain", ["auto", "one_launch", "chunks"])
 def test_north_star_1024_beds_sampled(monkeypatch, chain):
     """The north-star scale: 1024 beds; 64 beds spread over the range (first, last, and
     the chunk/tile boundaries in between) against the oracle, 2 ticks -- on the default path
-    (per-layer launches at this bed count) and with the K4c chain forced."""
-    if chain != "auto":
-        monkeypatch.setenv("HB_CHAIN", chain)
+    (per-layer launches at this bed count), the K4c chain as ONE launch over every bed, and the
+    chain over 64-bed chunks (HB_CHAIN_CHUNK_P=64, one launch each)."""
+    if chain == "one_launch":
+        monkeypatch.setenv("HB_CHAIN", "1")
+    elif chain == "chunks":
+        monkeypatch.setenv("HB_CHAIN_CHUNK_P", "64")
     beds = sorted(set(np.linspace(0, 1023, 62).astype(int).tolist()) | {511, 512})
     _run(Selector.from_indices(60, C2), 1024, 250, 2, 1, beds, zero_bed=511, check_every_tick=False)
 
@@ -336,6 +339,33 @@ def test_k4_cta_pairs_bit_identical(tmp_path):
 
 
 DEEP = [15, 19]   # w64-d16 (512-channel L = 59 / 30 layers), w128-d16 (1024-channel L = 59 / 30 layers)
+
+
+@pytest.mark.parametrize("agg", ["1", "0"])
+def test_chain_bed_chunks_bit_identical(tmp_path, agg):
+    """HB_CHAIN_CHUNK_P=64: above HB_CHAIN_MAX_P beds the chain runs one launch per bed chunk
+    (buffers reused, head partials and the fused aggregation per chunk, the ring cursor advanced
+    by the last chunk; opt-in, measured slower than the per-layer launches).  200 beds in chunks of 64 (the last one 8 beds + 56 padding rows) against
+    the per-layer launches and against one chain launch over every bed: bit-identical over two
+    sliding ticks, with the fused aggregation and with K5; sampled beds against the oracle."""
+    P, hop, ticks, seed = 200, 250, 2, 16
+    outs = {}
+    for name, env in (("chunks", {"HB_CHAIN_CHUNK_P": "64"}), ("layers", {"HB_CHAIN": "0"}),
+                      ("one", {"HB_CHAIN": "1", "HB_CHAIN_CHUNK_P": "0"})):
+        out = tmp_path / f"tick_{name}.npz"
+        e = dict(os.environ, HB_CHAIN_AGG=agg, **env)
+        subprocess.run([sys.executable, os.path.join(HERE, "_tick_worker.py"), str(out), str(P), str(hop),
+                        str(ticks), str(seed), ",".join(map(str, C2))], check=True, env=e, timeout=600)
+        outs[name] = np.load(out)
+    for other in ("layers", "one"):
+        for k in ("member_logits", "ens_prob", "ens_mean_logit"):
+            assert np.array_equal(outs["chunks"][k], outs[other][k]), (other, k)
+    got = outs["chunks"]
+    streams = synth.ecg_block(seed, P, 3, 0, W + ticks * hop)
+    beds = [0, 63, 64, 127, 128, 191, 192, 199]
+    ml, prob, mlog = cpu_path.cpu_tick(holmes_zoo(), Selector.from_indices(60, C2), streams, int(got["end"]),
+                                       beds=beds)
+    _compare(got["member_logits"][beds], got["ens_prob"][beds], got["ens_mean_logit"][beds], ml, prob, mlog)
 
 
 def test_k4_half_pairs_bit_identical(tmp_path):
