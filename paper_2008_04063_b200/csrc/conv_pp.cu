@@ -550,10 +550,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 //    depend on (target 2 * (epoch + 1): counters only grow, `epoch` counts
 //    finished launches of this chain, bumped by the last CTA to exit), then
 //    issues a proxy fence and the loads.  The epilogue's shortcut rows are
-//    read through L2 (ld.global.cg): they are written inside this launch.
+//    read through L2 (ld.global.cg): they are written inside this launch;
+//  * (ChainArgs::agg) the ensemble aggregation runs inside the launch: each
+//    half of a member's last-conv tile counts itself on a per-bed counter
+//    after its head partials are stored, and warp 3 (otherwise idle) of CTA
+//    p mod grid waits for bed p's count and sums the bed's partials in K5's
+//    order (bit-identical to the separate aggregate kernel).
 // Deadlock freedom: each CTA's list is sorted by layer and a layer only waits
 // on lower layers, so by induction on the layer index every item completes
-// (the grid is at most one CTA per SM, all resident).
+// (the grid is at most one CTA per SM, all resident); the aggregation only
+// waits on head tiles, which by the same induction all complete.
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
